@@ -1,0 +1,532 @@
+#!/usr/bin/env python
+"""Benchmark: PackMamba packed conv1d + selective scan, fwd + bwd, on B200.
+
+One step = conv1d_pack fwd -> ScanOp_pack fwd -> ScanOp_pack bwd ->
+conv1d_pack bwd on one layer's packed tensors (+ the NCCL all-reduce of the
+parameter gradients when N > 1), i.e. all of SURVEY §8(a) rows a1-a5.
+Default workload: BASELINE.json configs[2], the Mamba-1.4B layer shape
+(d_inner 4096, d_state 16, conv 4, pack 4096, 8 rows per GPU, bf16 I/O) with
+synthetic lognormal lengths [57, 2048] mean ~646 FIFO-packed.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+        torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Prints ONE JSON line on rank 0 (metric, value, roofline, cpu_baseline, e2e,
+clocks, ...).  The oracle (oracle/) is only used by the cpu_baseline leg and
+by --impl reference, never by the timed native path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workload  # noqa: E402
+
+METRIC = "scan+conv fwd+bwd packed tokens/s (1.4B shape) at 1/2/4/8 B200; % HBM peak"
+UNIT = "tokens/s"
+
+# minimal algorithmic lane-ops per (t, d, n) element of the scan kernels and
+# per (t, d) of the conv kernels; 1 MUFU ex2 counted as 1
+ALU_OPS = {"scan_fwd": 5, "scan_bwd": 15}
+
+
+def algo_bytes(Dn, N, isz):
+    """Algorithmic HBM bytes per packed slot for each kernel."""
+    return {
+        "conv_fwd": 2 * Dn * isz + 4,
+        "scan_fwd": 3 * Dn * isz + 2 * N * isz + 4,
+        "scan_bwd": 5 * Dn * isz + 2 * N * isz + 8 * N + 4,
+        "conv_bwd": 3 * Dn * isz + 4,
+    }
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return dict(hbm_gbs=float(p["hbm_gbs"]), sm_max_mhz=float(p.get("sm_max_mhz", 1965.0)),
+                    source="measured")
+    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback")
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.samples = []
+        self.proc = None
+        self.t_on = self.t_off = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu_id), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def mark_on(self):
+        self.t_on = time.time()
+
+    def mark_off(self):
+        self.t_off = time.time()
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        self.thread.join(timeout=2)
+        rows = []
+        for ts, line in self.samples:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            rows.append((ts, parts))
+        inside = [p for ts, p in rows if self.t_on and self.t_on - 0.06 <= ts <= self.t_off + 0.06]
+        use = inside if inside else rows
+        if not use:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[0]) for p in use if num(p[0]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in use for i in range(4) if p[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": num(use[0][1]), "reasons": reasons,
+                "samples": len(use), "samples_in_timed_region": len(inside),
+                "power_w_max": max((num(p[2]) or 0.0) for p in use)}
+
+
+# ---------------------------------------------------------------------------
+# workload construction (seeded by global row id -> identical rows for any N)
+# ---------------------------------------------------------------------------
+
+def build_layout(cfg, total_rows):
+    """Draw lengths (P:246 distribution) and FIFO-pack them with the
+    product planner; return per-row length lists for the first total_rows
+    sealed rows."""
+    import paper_2408_03865_b200 as pm
+    n = max(64, int(total_rows * cfg.L / 600) + 64)
+    while True:
+        lens = workload.lengths_stream(cfg.name, n)
+        row, off, nr = pm.pm_plan_fifo(lens, cfg.L)
+        if nr - 1 >= total_rows:  # the last row may be unsealed: drop it
+            break
+        n *= 2
+    keep = row < total_rows
+    return lens[keep], row[keep], off[keep]
+
+
+def setup_native(torch, cfg, rank, world, dev):
+    import paper_2408_03865_b200 as pm
+    from paper_2408_03865_b200.dp import ParamGrads, shard_rows
+
+    total = cfg.R * world
+    rows_g = list(shard_rows(total, rank, world))
+    lens, row, off = build_layout(cfg, total)
+    # pm_pack the token ids of this rank's rows (data-loader step, untimed)
+    mine = (row >= rows_g[0]) & (row <= rows_g[-1])
+    lens_m = lens[mine]
+    tok = torch.arange(int(lens_m.sum()), dtype=torch.int32, device=dev)
+    ids, pos, prow, poff = pm.pm_pack(lens_m, cfg.L, tok)
+    assert ids.shape[0] == cfg.R, (ids.shape, cfg.R)
+    rows_layout = workload.rows_from_plan(lens_m, prow, poff, cfg.R)
+    _, valid = workload.pos_from_rows(rows_layout, cfg.L)
+    T = workload.row_tensors(torch, cfg, rows_g, valid, device=dev)
+    P = workload.params(torch, cfg, device=dev)
+    pad = 1.0 - float(valid.mean())
+    return dict(pos=pos, T=T, P=P, valid=valid, rows_layout=rows_layout, pad=pad,
+                lens=lens_m, ParamGrads=ParamGrads)
+
+
+class Step:
+    """Preallocated buffers + the 4-kernel step through the public API."""
+
+    def __init__(self, torch, cfg, D, dev, world, dist):
+        import paper_2408_03865_b200 as pm
+        self.pm, self.torch, self.cfg, self.dist, self.world = pm, torch, cfg, dist, world
+        self.D = D
+        T, P = D["T"], D["P"]
+        R, L, Dn, N, K = cfg.R, cfg.L, cfg.Dn, cfg.N, cfg.K
+        self.u = torch.empty_like(T["x"])
+        self.y = torch.empty_like(T["x"])
+        self.states = torch.empty(pm.pm_selective_scan_state_bytes(R, Dn, L, N) // 4,
+                                  dtype=torch.float32, device=dev)
+        self.pg = D["ParamGrads"](torch, Dn, N, K, dev)
+        f32 = dict(dtype=torch.float32, device=dev)
+        self.g = dict(du=torch.empty_like(T["x"]), ddt=torch.empty_like(T["x"]),
+                      dA=self.pg["dA"], dB=torch.empty((R, N, L), **f32),
+                      dC=torch.empty((R, N, L), **f32), dD=self.pg["dD"],
+                      ddt_bias=self.pg["ddt_bias"])
+        self.dx = torch.empty_like(T["x"])
+        self.ws_scan = torch.empty(pm.pm_selective_scan_bwd_workspace(R, Dn, L, N),
+                                   dtype=torch.uint8, device=dev)
+        self.ws_conv = torch.empty(pm.pm_causal_conv1d_bwd_workspace(R, Dn, L, K),
+                                   dtype=torch.uint8, device=dev)
+        self.events = None
+
+    def kernels(self, ev=None):
+        pm, T, P, pos = self.pm, self.D["T"], self.D["P"], self.D["pos"]
+
+        def mark(i):
+            if ev is not None:
+                ev[i].record()
+        mark(0)
+        pm.pm_causal_conv1d_fwd(T["x"], P["w"], P["bias"], pos, out=self.u, silu=True)
+        mark(1)
+        pm.pm_selective_scan_fwd(self.u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
+                                 pos, y=self.y, states=self.states)
+        mark(2)
+        pm.pm_selective_scan_bwd(self.u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
+                                 pos, T["dy"], states=self.states, out=self.g,
+                                 workspace=self.ws_scan)
+        mark(3)
+        pm.pm_causal_conv1d_bwd(T["x"], P["w"], P["bias"], pos, self.g["du"], dx=self.dx,
+                                dw=self.pg["dw"], dbias=self.pg["db"], workspace=self.ws_conv)
+        mark(4)
+        if self.world > 1:
+            self.pg.allreduce(self.dist)
+        mark(5)
+
+    LAUNCHES_PER_STEP = 7  # conv_fwd 1, scan_fwd 1, scan_bwd 3, conv_bwd 2 (NCCL not counted)
+
+
+def max_over_ranks(torch, dist, world, v, dev):
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle legs
+# ---------------------------------------------------------------------------
+
+def oracle_step(orc, cfg, sample):
+    """One oracle pass of the full path on a bounded sample (host fp64)."""
+    x, dt, B, C, dy, pos, P, Dc = sample
+    u = orc.conv_fwd(x, P["w"][:Dc], P["bias"][:Dc], pos)
+    orc.scan_fwd(u, dt, P["A"][:Dc], B, C, P["D"][:Dc], P["dt_bias"][:Dc], pos)
+    g = orc.scan_bwd(u, dt, P["A"][:Dc], B, C, P["D"][:Dc], P["dt_bias"][:Dc], pos, dy)
+    orc.conv_bwd(x, P["w"][:Dc], P["bias"][:Dc], pos, g["du"])
+
+
+def oracle_sample(torch, cfg, Dc, rows_layout):
+    """Row 0 of the workload, first Dc channels, as exact fp64 host arrays.
+    Inputs come from the seeded generator (never from the CUDA path)."""
+    pos, valid = workload.pos_from_rows(rows_layout[:1], cfg.L)
+    sub = workload.Shape(cfg.name, 1, cfg.L, cfg.Dn, cfg.N, cfg.K, cfg.dtype)
+    T = workload.row_tensors(torch, sub, [0], valid, device="cpu")
+    P = {k: v.double().numpy() for k, v in workload.params(torch, cfg, device="cpu").items()}
+    f = lambda t: t.double().numpy()
+    return (f(T["x"])[:, :Dc].copy(), f(T["dt"])[:, :Dc].copy(), f(T["B"]), f(T["C"]),
+            f(T["dy"])[:, :Dc].copy(), pos, P, Dc)
+
+
+def cpu_time_per_channel(torch, orc, cfg, rows_layout, Dc=16):
+    s = oracle_sample(torch, cfg, Dc, rows_layout)
+    t0 = time.perf_counter()
+    oracle_step(orc, cfg, s)
+    return (time.perf_counter() - t0) / Dc
+
+
+def cpu_baseline(torch, cfg, target_s=12.0):
+    import oracle as orc
+    lens, row, off = build_layout_host(cfg)  # oracle planner: no input from the CUDA path
+    rows_layout = workload.rows_from_plan(lens, row, off, cfg.R)
+    per_ch = cpu_time_per_channel(torch, orc, cfg, rows_layout)
+    Dc = int(max(16, min(cfg.Dn, target_s / max(per_ch, 1e-9))))
+    s = oracle_sample(torch, cfg, Dc, rows_layout)
+    t0 = time.perf_counter()
+    oracle_step(orc, cfg, s)
+    dt = time.perf_counter() - t0
+    slots = cfg.L * Dc / cfg.Dn  # channel-fraction-scaled slots of the sample
+    return {"value": slots / dt, "unit": UNIT, "cores": orc.num_threads(), "kind": "oracle",
+            "sample": f"1 row x {Dc} of {cfg.Dn} channels x L={cfg.L} (conv fwd, scan fwd, "
+                      f"scan bwd, conv bwd in fp64), {dt:.1f} s, slots scaled by "
+                      f"{Dc}/{cfg.Dn}"}
+
+
+def run_reference(args, cfg):
+    """--impl reference: the fp64 oracle on this workload, timed on host cores."""
+    import torch
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as orc
+    lens, row, off = build_layout_host(cfg)
+    rows_layout = workload.rows_from_plan(lens, row, off, cfg.R)
+    per_ch = cpu_time_per_channel(torch, orc, cfg, rows_layout)
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    Dc = int(max(16, min(cfg.Dn, budget / max(per_ch, 1e-9))))
+    s = oracle_sample(torch, cfg, Dc, rows_layout)
+    for _ in range(args.warmup):
+        oracle_step(orc, cfg, s)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(orc, cfg, s)
+    el = (time.perf_counter() - t0) / args.steps
+    slots = cfg.L * Dc / cfg.Dn
+    v = slots / el
+    sample = (f"1 row x {Dc} of {cfg.Dn} channels x L={cfg.L} per step (fp64 oracle: conv fwd, "
+              f"scan fwd, scan bwd, conv bwd), slots scaled by {Dc}/{cfg.Dn}")
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": el * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"{cfg.name}: R={cfg.R} L={cfg.L} Dn={cfg.Dn} N={cfg.N} "
+                                  f"K={cfg.K}", "io": cfg.dtype},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": orc.num_threads(),
+                            "kind": "oracle", "sample": sample},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def build_layout_host(cfg):
+    """Host-only layout for the reference leg (oracle planner, same seed)."""
+    import oracle as orc
+    n = max(64, int(cfg.R * cfg.L / 600) + 64)
+    while True:
+        lens = workload.lengths_stream(cfg.name, n)
+        row, off, nr = orc.plan_fifo(lens, cfg.L)
+        if nr - 1 >= cfg.R:
+            break
+        n *= 2
+    keep = row < cfg.R
+    return lens[keep], row[keep], off[keep]
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="1.4b", choices=sorted(workload.CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    cfg = workload.CONFIGS[args.config]
+
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    D = setup_native(torch, cfg, rank, world, dev)
+    step = Step(torch, cfg, D, dev, world, dist)
+    isz = 2 if cfg.dtype == "bf16" else 4
+    peaks = load_peaks()
+
+    props = torch.cuda.get_device_properties(dev)
+    gpu_id = local
+    try:
+        gpu_id = f"{props.pci_domain_id:08X}:{props.pci_bus_id:02X}:{props.pci_device_id:02X}.0"
+    except AttributeError:
+        pass
+    clocks = ClockSampler(gpu_id)
+    clocks.start()
+
+    for _ in range(args.warmup):
+        step.kernels()
+    torch.cuda.synchronize()
+
+    # ---- timed region: exactly K steps, barrier + sync on both sides ----
+    nk = 5
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.mark_on()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record()
+    for i in range(args.steps):
+        step.kernels(evs[i])
+    t_end.record()
+    torch.cuda.synchronize()
+    clocks.mark_off()
+    if world > 1:
+        dist.barrier()
+    ms_local = t_start.elapsed_time(t_end) / args.steps
+    ms = max_over_ranks(torch, dist, world, ms_local, dev)
+    names = ["conv_fwd", "scan_fwd", "scan_bwd", "conv_bwd", "allreduce"]
+    kms = {n: float(np.mean([evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(args.steps)]))
+           for j, n in enumerate(names)}
+    clk = clocks.stop()
+
+    slots_rank = cfg.R * cfg.L
+    total_slots = slots_rank * world
+    value = total_slots / (ms * 1e-3)
+    ab = algo_bytes(cfg.Dn, cfg.N, isz)
+    step_bytes = sum(ab.values()) * slots_rank
+    hbm_frac_step = step_bytes / (ms_local * 1e-3) / (peaks["hbm_gbs"] * 1e9)
+    kern = {}
+    for n in names[:4]:
+        t = kms[n] * 1e-3
+        gbs = ab[n] * slots_rank / t / 1e9
+        kern[n] = {"ms": kms[n], "share": kms[n] / ms_local, "hbm_gbs": gbs,
+                   "hbm_frac": gbs / peaks["hbm_gbs"]}
+        if n in ALU_OPS:
+            ops = ALU_OPS[n] * slots_rank * cfg.Dn * cfg.N
+            peak_ops = 148 * 128 * peaks["sm_max_mhz"] * 1e6
+            kern[n]["alu_gops"] = ops / t / 1e9
+            kern[n]["alu_frac"] = ops / t / peak_ops
+    if world > 1:
+        kern["allreduce"] = {"ms": kms["allreduce"], "share": kms["allreduce"] / ms_local,
+                             "bytes": step.pg.nbytes}
+    dom = max(names[:4], key=lambda n: kms[n])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr = json.load(f).get(cfg.name, {})
+        traffic = tr.get(dom)
+    if dom in ALU_OPS:
+        roof = {"bound": "alu", "achieved": kern[dom]["alu_gops"],
+                "peak": 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e9, "unit": "Gop/s",
+                "frac": kern[dom]["alu_frac"], "traffic": traffic, "kernel": dom,
+                "peak_source": f"148 SMs x 128 FP32/issue lanes x {peaks['sm_max_mhz']:.0f} MHz "
+                               "(guide unit counts, MEASURED_PEAKS sm_max_mhz)",
+                "hbm_gbs": kern[dom]["hbm_gbs"], "hbm_frac": kern[dom]["hbm_frac"]}
+    else:
+        roof = {"bound": "hbm", "achieved": kern[dom]["hbm_gbs"], "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": kern[dom]["hbm_frac"], "traffic": traffic,
+                "kernel": dom, "peak_source": peaks["source"]}
+
+    # ---- e2e: same step through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(torch, step, D, dist, world, dev, args.e2e_steps, total_slots)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(torch, cfg)
+        except Exception as e:  # never lose the GPU line over the baseline
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle",
+                   "sample": f"failed: {e!r}"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": cfg.dtype, "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: Mamba layer shape R={cfg.R} rows/GPU x "
+                                   f"L={cfg.L}, d_inner={cfg.Dn}, d_state={cfg.N}, conv={cfg.K}",
+                       "global_rows": cfg.R * world, "io_dtype": cfg.dtype,
+                       "lengths": "lognormal [57,2048] mean~646 (P:246), FIFO-packed (P:273)",
+                       "padding_rate": D["pad"], "parallelism": f"dp{world} (row-sharded)",
+                       "l2": "inputs larger than L2 (256 MiB per (R,Dn,L) tensor)"},
+            "real_tokens_per_s": value * (1 - D["pad"]),
+            "hbm_frac_step": hbm_frac_step,
+            "hbm_peak_gbs": peaks["hbm_gbs"], "peak_source": peaks["source"],
+            "roofline": roof, "kernels": kern, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clk, "gpu_launches": Step.LAUNCHES_PER_STEP * args.steps,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(torch, step, D, dist, world, dev, n, total_slots):
+    """Host (pinned) -> device inputs, the 4 kernels (+allreduce), device ->
+    host of dx and the parameter gradients, every step, timed with events."""
+    T, pos = D["T"], D["pos"]
+    host = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in T.items()}
+    for k in host:
+        host[k].copy_(T[k].cpu())
+    hpos = torch.empty(pos.shape, dtype=pos.dtype, pin_memory=True)
+    hpos.copy_(pos.cpu())
+    hdx = torch.empty(step.dx.shape, dtype=step.dx.dtype, pin_memory=True)
+    hpg = torch.empty(step.pg.flat.shape, dtype=torch.float32, pin_memory=True)
+    h2d = sum(v.numel() * v.element_size() for v in host.values()) + hpos.numel() * 4
+    d2h = hdx.numel() * hdx.element_size() + hpg.numel() * 4
+
+    def one():
+        for k in host:
+            T[k].copy_(host[k], non_blocking=True)
+        pos.copy_(hpos, non_blocking=True)
+        step.kernels()
+        hdx.copy_(step.dx, non_blocking=True)
+        hpg.copy_(step.pg.flat, non_blocking=True)
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(n):
+        one()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / n
+    ms = max_over_ranks(torch, dist, world, ms, dev)
+    return {"value": total_slots / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": n,
+            "api": "paper_2408_03865_b200.pm_* (C ABI) with pinned host buffers"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

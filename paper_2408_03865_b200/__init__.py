@@ -1,0 +1,305 @@
+"""PackMamba (arXiv 2408.03865) packed conv1d + selective scan on B200.
+
+Thin ctypes binding over ``libpm.so`` (the C ABI in ``include/pm.h``).  Every
+function here only marshals arguments -- tensor data pointers, sizes, the
+current CUDA stream -- into the same-named C entry point; all computation
+runs in the library's sm_100a kernels.  There is no CPU fallback: if the
+library is missing or the tensors are not on a CUDA device, calls raise.
+
+PyTorch is used for device memory, streams and process groups only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = [
+    "PMError", "lib", "pm_status_string", "pm_plan_fifo", "pm_plan_greedy",
+    "pm_pack", "pm_pack_planned", "pm_causal_conv1d_fwd", "pm_causal_conv1d_bwd",
+    "pm_causal_conv1d_bwd_workspace", "pm_selective_scan_state_bytes",
+    "pm_selective_scan_fwd", "pm_selective_scan_bwd",
+    "pm_selective_scan_bwd_workspace", "EXPORTED_SYMBOLS",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpm.so")
+
+PM_F32, PM_BF16 = 0, 1
+STATUS = {0: "PM_OK", 1: "PM_ERR_INVALID_ARG", 2: "PM_ERR_CAPACITY", 3: "PM_ERR_SHAPE",
+          4: "PM_ERR_DTYPE", 5: "PM_ERR_ALIGN", 6: "PM_ERR_UNSUPPORTED", 7: "PM_ERR_CUDA",
+          8: "PM_ERR_WORKSPACE"}
+
+# every symbol include/pm.h declares (checked by tests/test_abi.py)
+EXPORTED_SYMBOLS = [
+    "pm_status_string", "pm_version", "pm_plan_fifo", "pm_plan_greedy", "pm_pack",
+    "pm_pack_planned", "pm_causal_conv1d_fwd", "pm_causal_conv1d_bwd_workspace",
+    "pm_causal_conv1d_bwd", "pm_selective_scan_state_bytes", "pm_selective_scan_fwd",
+    "pm_selective_scan_bwd_workspace", "pm_selective_scan_bwd",
+]
+
+
+class PMError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        self.name = STATUS.get(code, str(code))
+        super().__init__(f"{where}: {self.name} ({pm_status_string(code)})")
+
+
+_vp, _i64, _i32, _sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+_lib = None
+
+
+def lib():
+    """Load libpm.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            from . import _build
+            _build.build()
+        L = ctypes.CDLL(LIB_PATH)
+        L.pm_status_string.restype = ctypes.c_char_p
+        L.pm_status_string.argtypes = [ctypes.c_int]
+        L.pm_version.restype = ctypes.c_char_p
+        for f in ("pm_plan_fifo", "pm_plan_greedy"):
+            getattr(L, f).argtypes = [_vp, _i64, _i64, _vp, _vp, _vp]
+        L.pm_pack.argtypes = [_vp, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp]
+        L.pm_pack_planned.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp]
+        L.pm_causal_conv1d_fwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i32,
+                                           ctypes.c_int, _i32, _vp]
+        L.pm_causal_conv1d_bwd_workspace.restype = _sz
+        L.pm_causal_conv1d_bwd_workspace.argtypes = [_i64, _i64, _i64, _i32]
+        L.pm_causal_conv1d_bwd.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64,
+                                           _i64, _i32, ctypes.c_int, _i32, _vp, _sz, _vp]
+        L.pm_selective_scan_state_bytes.restype = _sz
+        L.pm_selective_scan_state_bytes.argtypes = [_i64, _i64, _i64, _i32]
+        L.pm_selective_scan_fwd.argtypes = [_vp] * 7 + [_i32, _vp, _vp, _vp, _i64, _i64, _i64,
+                                                       _i32, ctypes.c_int, _vp]
+        L.pm_selective_scan_bwd_workspace.restype = _sz
+        L.pm_selective_scan_bwd_workspace.argtypes = [_i64, _i64, _i64, _i32, _i32]
+        L.pm_selective_scan_bwd.argtypes = ([_vp] * 7 + [_i32] + [_vp] * 10 + [_vp, _sz] +
+                                            [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
+        for f in EXPORTED_SYMBOLS:
+            if f not in ("pm_status_string", "pm_version") and not f.endswith(
+                    ("_workspace", "_bytes")):
+                getattr(L, f).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def pm_status_string(code: int) -> str:
+    return lib().pm_status_string(int(code)).decode()
+
+
+def _check(rc: int, where: str) -> None:
+    if rc != 0:
+        raise PMError(rc, where)
+
+
+# ----------------------------------------------------------------------------
+# marshalling helpers
+# ----------------------------------------------------------------------------
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(t):
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _io(t):
+    import torch
+    if t.dtype == torch.float32:
+        return PM_F32
+    if t.dtype == torch.bfloat16:
+        return PM_BF16
+    raise TypeError(f"unsupported I/O dtype {t.dtype} (float32 or bfloat16)")
+
+
+def _dev(*ts):
+    for t in ts:
+        if t is not None:
+            if not t.is_cuda:
+                raise RuntimeError("libpm runs on CUDA tensors only (no CPU fallback)")
+            if not t.is_contiguous():
+                raise RuntimeError("libpm needs contiguous tensors")
+
+
+def _host_i32(a):
+    import numpy as np
+    a = np.ascontiguousarray(a, dtype=np.int32)
+    return a, a.ctypes.data_as(ctypes.c_void_p)
+
+
+# ----------------------------------------------------------------------------
+# packing
+# ----------------------------------------------------------------------------
+
+def pm_plan_fifo(seq_lens, pack_len):
+    """FIFO-seal plan on the host -> (seq_row, seq_off, n_rows)."""
+    return _plan("pm_plan_fifo", seq_lens, pack_len)
+
+
+def pm_plan_greedy(seq_lens, pack_len):
+    """First-fit-decreasing plan (P:273 'local greedy') -> (row, off, n_rows)."""
+    return _plan("pm_plan_greedy", seq_lens, pack_len)
+
+
+def _plan(name, seq_lens, pack_len):
+    import numpy as np
+    lens, lp = _host_i32(seq_lens)
+    n = lens.shape[0]
+    row = np.zeros(max(n, 1), np.int64)
+    off = np.zeros(max(n, 1), np.int64)
+    nr = np.zeros(1, np.int64)
+    _check(getattr(lib(), name)(lp, n, int(pack_len), row.ctypes.data, off.ctypes.data,
+                                nr.ctypes.data), name)
+    return row[:n], off[:n], int(nr[0])
+
+
+def pm_pack(seq_lens, pack_len, src, dst=None, pos=None, max_rows=None):
+    """Pack token-major records ``src`` (sum(len), ...) on the GPU.
+
+    Returns (dst, pos, seq_row, seq_off).  ``dst``/``pos`` are allocated when
+    not given: dst (n_rows, pack_len, *src.shape[1:]) like src, pos int32."""
+    import numpy as np
+    import torch
+    _dev(src)
+    lens, lp = _host_i32(seq_lens)
+    n = lens.shape[0]
+    rec = src.element_size() * (src[0].numel() if src.dim() > 1 else 1)
+    row = np.zeros(max(n, 1), np.int64)
+    off = np.zeros(max(n, 1), np.int64)
+    nr = np.zeros(1, np.int64)
+    L = lib()
+    if dst is None or pos is None:
+        _check(L.pm_pack(lp, n, int(pack_len), None, rec, None, None, 0, nr.ctypes.data,
+                         None, None, None), "pm_pack(query)")
+        rows = int(nr[0])
+        dst = torch.empty((rows, pack_len, *src.shape[1:]), dtype=src.dtype, device=src.device)
+        pos = torch.empty((rows, pack_len), dtype=torch.int32, device=src.device)
+    _dev(dst, pos)
+    mr = dst.shape[0] if max_rows is None else int(max_rows)
+    _check(L.pm_pack(lp, n, int(pack_len), _ptr(src), rec, _ptr(dst), _ptr(pos), mr,
+                     nr.ctypes.data, row.ctypes.data, off.ctypes.data, _stream(src)), "pm_pack")
+    return dst, pos, row[:n], off[:n]
+
+
+def pm_pack_planned(seq_lens, pack_len, seq_row, seq_off, n_rows, src, dst, pos):
+    import numpy as np
+    _dev(src, dst, pos)
+    lens, lp = _host_i32(seq_lens)
+    row = np.ascontiguousarray(seq_row, dtype=np.int64)
+    off = np.ascontiguousarray(seq_off, dtype=np.int64)
+    rec = src.element_size() * (src[0].numel() if src.dim() > 1 else 1)
+    _check(lib().pm_pack_planned(lp, lens.shape[0], int(pack_len), row.ctypes.data,
+                                 off.ctypes.data, int(n_rows), _ptr(src), rec, _ptr(dst),
+                                 _ptr(pos), _stream(src)), "pm_pack_planned")
+    return dst, pos
+
+
+# ----------------------------------------------------------------------------
+# conv1d_pack
+# ----------------------------------------------------------------------------
+
+def pm_causal_conv1d_fwd(x, w, bias, pos, out=None, silu=True):
+    """Alg 1 conv1d_pack forward: x (R,Dn,L) f32|bf16, w (Dn,K) f32, pos (R,L) i32."""
+    import torch
+    _dev(x, w, bias, pos)
+    R, Dn, L = x.shape
+    out = torch.empty_like(x) if out is None else out
+    _dev(out)
+    _check(lib().pm_causal_conv1d_fwd(_ptr(x), _ptr(w), _ptr(bias), _ptr(pos), _ptr(out), R, Dn,
+                                      L, w.shape[1], _io(x), int(bool(silu)), _stream(x)),
+           "pm_causal_conv1d_fwd")
+    return out
+
+
+def pm_causal_conv1d_bwd_workspace(R, Dn, L, K):
+    return int(lib().pm_causal_conv1d_bwd_workspace(R, Dn, L, K))
+
+
+def pm_causal_conv1d_bwd(x, w, bias, pos, dout, dx=None, dw=None, dbias=None, silu=True,
+                         workspace=None):
+    """Adjoint of conv1d_pack -> (dx, dw, dbias)."""
+    import torch
+    _dev(x, w, bias, pos, dout)
+    R, Dn, L = x.shape
+    K = w.shape[1]
+    dx = torch.empty_like(x) if dx is None else dx
+    dw = torch.empty_like(w) if dw is None else dw
+    if dbias is None and bias is not None:
+        dbias = torch.empty_like(bias)
+    need = pm_causal_conv1d_bwd_workspace(R, Dn, L, K)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=x.device)
+    _dev(dx, dw, dbias, workspace)
+    _check(lib().pm_causal_conv1d_bwd(_ptr(x), _ptr(w), _ptr(bias), _ptr(pos), _ptr(dout),
+                                      _ptr(dx), _ptr(dw), _ptr(dbias), R, Dn, L, K, _io(x),
+                                      int(bool(silu)), _ptr(workspace), workspace.numel(),
+                                      _stream(x)), "pm_causal_conv1d_bwd")
+    return dx, dw, dbias
+
+
+# ----------------------------------------------------------------------------
+# ScanOp_pack
+# ----------------------------------------------------------------------------
+
+def pm_selective_scan_state_bytes(R, Dn, L, N):
+    return int(lib().pm_selective_scan_state_bytes(R, Dn, L, N))
+
+
+def pm_selective_scan_bwd_workspace(R, Dn, L, N, recompute_states=False):
+    return int(lib().pm_selective_scan_bwd_workspace(R, Dn, L, N, int(bool(recompute_states))))
+
+
+def pm_selective_scan_fwd(u, dt, A, B, C, Dskip, dt_bias, pos, y=None, states=None,
+                          dt_softplus=True, want_states=True):
+    """ScanOp_pack forward (Alg 2; Eq 1a/1b/2a).  Returns (y, states)."""
+    import torch
+    _dev(u, dt, A, B, C, Dskip, dt_bias, pos)
+    R, Dn, L = u.shape
+    N = A.shape[1]
+    y = torch.empty_like(u) if y is None else y
+    if states is None and want_states:
+        nb = pm_selective_scan_state_bytes(R, Dn, L, N)
+        states = torch.empty(nb // 4, dtype=torch.float32, device=u.device)
+    _dev(y, states)
+    _check(lib().pm_selective_scan_fwd(_ptr(u), _ptr(dt), _ptr(A), _ptr(B), _ptr(C),
+                                       _ptr(Dskip), _ptr(dt_bias), int(bool(dt_softplus)),
+                                       _ptr(pos), _ptr(y), _ptr(states), R, Dn, L, N, _io(u),
+                                       _stream(u)), "pm_selective_scan_fwd")
+    return y, states
+
+
+def pm_selective_scan_bwd(u, dt, A, B, C, Dskip, dt_bias, pos, dy, states=None,
+                          dt_softplus=True, out=None, workspace=None):
+    """Adjoint of ScanOp_pack.  Returns dict du, ddt, dA, dB, dC, dD, ddt_bias.
+
+    ``out`` may supply preallocated outputs (same keys)."""
+    import torch
+    _dev(u, dt, A, B, C, Dskip, dt_bias, pos, dy, states)
+    R, Dn, L = u.shape
+    N = A.shape[1]
+    o = dict(out or {})
+    dev = u.device
+    f32 = dict(dtype=torch.float32, device=dev)
+    o.setdefault("du", torch.empty_like(u))
+    o.setdefault("ddt", torch.empty_like(u))
+    o.setdefault("dA", torch.empty((Dn, N), **f32))
+    o.setdefault("dB", torch.empty((R, N, L), **f32))
+    o.setdefault("dC", torch.empty((R, N, L), **f32))
+    o.setdefault("dD", torch.empty((Dn,), **f32) if Dskip is not None else None)
+    o.setdefault("ddt_bias", torch.empty((Dn,), **f32) if dt_bias is not None else None)
+    need = pm_selective_scan_bwd_workspace(R, Dn, L, N, states is None)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    _dev(workspace, *[v for v in o.values() if v is not None])
+    _check(lib().pm_selective_scan_bwd(
+        _ptr(u), _ptr(dt), _ptr(A), _ptr(B), _ptr(C), _ptr(Dskip), _ptr(dt_bias),
+        int(bool(dt_softplus)), _ptr(pos), _ptr(states), _ptr(dy), _ptr(o["du"]), _ptr(o["ddt"]),
+        _ptr(o["dA"]), _ptr(o["dB"]), _ptr(o["dC"]), _ptr(o["dD"]), _ptr(o["ddt_bias"]),
+        _ptr(workspace), workspace.numel(), R, Dn, L, N, _io(u), _stream(u)),
+        "pm_selective_scan_bwd")
+    return o

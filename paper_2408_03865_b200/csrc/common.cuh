@@ -1,0 +1,177 @@
+// common.cuh -- device helpers shared by libpm's sm_100a kernels.
+// (Product path.  Shares nothing with oracle/.)
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pm.h"
+
+#define PM_DEV __device__ __forceinline__
+
+namespace pm {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+// ---------------------------------------------------------------- math ----
+PM_DEV float ex2(float x) {  // MUFU.EX2 (flush-to-zero)
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+PM_DEV float rcp(float x) {  // MUFU.RCP
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+PM_DEV float sigmoidf_fast(float v) { return rcp(1.f + ex2(-v * kLog2e)); }
+
+// softplus(v) = log(1 + e^v); linear tail above 20 (error < 2e-9 relative,
+// reading Q4).  log1pf keeps full fp32 accuracy for small e^v (delta ~1e-4).
+PM_DEV float softplusf(float v) { return v > 20.f ? v : log1pf(ex2(v * kLog2e)); }
+
+// ----------------------------------------------------------------- I/O ----
+template <typename T> struct IO;
+template <> struct IO<float> {
+  static PM_DEV float ld(const float* p) { return __ldg(p); }
+  static PM_DEV void st(float* p, float v) { *p = v; }
+  static constexpr int kIsz = 4;
+};
+template <> struct IO<__nv_bfloat16> {
+  static PM_DEV float ld(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+  static PM_DEV void st(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+  static constexpr int kIsz = 2;
+};
+
+// Load 8 consecutive elements p[i..i+7] of a row of length n (elements
+// outside [0, n) read as 0).  kVec: caller guarantees 16-byte alignment of
+// p + i whenever i % 8 == 0 and the whole vector is inside the row.
+template <typename T, bool kVec>
+PM_DEV void load8(const T* __restrict__ p, int64_t i, int64_t n, float (&v)[8]) {
+  if (kVec && i >= 0 && i + 8 <= n) {
+    if constexpr (sizeof(T) == 2) {
+      uint4 q = __ldg(reinterpret_cast<const uint4*>(p + i));
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float2 f = __bfloat1622float2(b[k]);
+        v[2 * k] = f.x;
+        v[2 * k + 1] = f.y;
+      }
+    } else {
+      float4 a = __ldg(reinterpret_cast<const float4*>(p + i));
+      float4 b = __ldg(reinterpret_cast<const float4*>(p + i + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      v[k] = (i + k >= 0 && i + k < n) ? IO<T>::ld(p + i + k) : 0.f;
+  }
+}
+
+// Store v[k] to p[i+k] for the k with lo <= i+k < hi.
+template <typename T, bool kVec>
+PM_DEV void store8(T* __restrict__ p, int64_t i, int64_t lo, int64_t hi, const float (&v)[8]) {
+  if (kVec && i >= lo && i + 8 <= hi) {
+    if constexpr (sizeof(T) == 2) {
+      uint4 q;
+      __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) b[k] = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+      *reinterpret_cast<uint4*>(p + i) = q;
+    } else {
+      *reinterpret_cast<float4*>(p + i) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4*>(p + i + 4) = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (i + k >= lo && i + k < hi) IO<T>::st(p + i + k, v[k]);
+  }
+}
+
+// Load 4 consecutive elements (same contract as load8 with 4).
+template <typename T, bool kVec>
+PM_DEV void load4(const T* __restrict__ p, int64_t i, int64_t n, float (&v)[4]) {
+  if (kVec && i >= 0 && i + 4 <= n) {
+    if constexpr (sizeof(T) == 2) {
+      uint2 q = __ldg(reinterpret_cast<const uint2*>(p + i));
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+      float2 f0 = __bfloat1622float2(b[0]), f1 = __bfloat1622float2(b[1]);
+      v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
+    } else {
+      float4 a = __ldg(reinterpret_cast<const float4*>(p + i));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      v[k] = (i + k >= 0 && i + k < n) ? IO<T>::ld(p + i + k) : 0.f;
+  }
+}
+
+template <typename T, bool kVec>
+PM_DEV void store4(T* __restrict__ p, int64_t i, int64_t lo, int64_t hi, const float (&v)[4]) {
+  if (kVec && i >= lo && i + 4 <= hi) {
+    if constexpr (sizeof(T) == 2) {
+      uint2 q;
+      __nv_bfloat162* b = reinterpret_cast<__nv_bfloat162*>(&q);
+      b[0] = __floats2bfloat162_rn(v[0], v[1]);
+      b[1] = __floats2bfloat162_rn(v[2], v[3]);
+      *reinterpret_cast<uint2*>(p + i) = q;
+    } else {
+      *reinterpret_cast<float4*>(p + i) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (i + k >= lo && i + k < hi) IO<T>::st(p + i + k, v[k]);
+  }
+}
+
+// --------------------------------------------------- segment splitting ----
+// A packed row is a concatenation of independent sequences (no
+// sequence spans rows; the reset at heads cuts every carry).  So a row can
+// be split at heads into independent time segments without any carry
+// fix-up.  Segment k of nseg covers [b_k, b_{k+1}) where b_0 = 0,
+// b_nseg = L and b_k = first head at or after k*ceil(L/nseg).  Boundaries
+// are monotone; a segment may be empty.  All threads of the block call this.
+PM_DEV int first_head_from(const int32_t* __restrict__ pos_row, int L, int t0, int* s_red) {
+  // block-cooperative search for min{t >= t0 : pos[t] == 0} (or L)
+  if (t0 >= L) return L;
+  if (t0 <= 0) return 0;
+  int found = L;
+  for (int base = t0; base < L; base += blockDim.x) {
+    int t = base + threadIdx.x;
+    int hit = (t < L && __ldg(pos_row + t) == 0) ? t : L;
+    // block min
+    for (int o = 16; o > 0; o >>= 1) hit = min(hit, __shfl_xor_sync(0xffffffffu, hit, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = hit;
+    __syncthreads();
+    int m = L;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = min(m, s_red[w]);
+    if (m < L) { found = m; break; }
+  }
+  __syncthreads();
+  return found;
+}
+
+PM_DEV void segment_bounds(const int32_t* __restrict__ pos_row, int L, int k, int nseg,
+                           int* s_red, int& s0, int& s1) {
+  const int seg = (L + nseg - 1) / nseg;
+  s0 = (k == 0) ? 0 : first_head_from(pos_row, L, k * seg, s_red);
+  s1 = (k == nseg - 1) ? L : first_head_from(pos_row, L, (k + 1) * seg, s_red);
+}
+
+}  // namespace pm
+
+// host-side error helper
+#define PM_LAUNCH_CHECK()                                     \
+  do {                                                        \
+    if (cudaGetLastError() != cudaSuccess) return PM_ERR_CUDA; \
+  } while (0)

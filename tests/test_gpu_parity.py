@@ -1,0 +1,244 @@
+"""GPU parity: every kernel of the hot path vs the fp64 oracle, called
+through the C ABI (paper_2408_03865_b200 -> libpm.so).
+
+Per-kernel protocol: the oracle is fed exactly the tensors
+the GPU kernel consumed (converted exactly to fp64), so one kernel's
+rounding is not charged to the next.  Tolerances are north_star's, written
+in tests/_common.TOL; the metric is reading Q14.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import paper_2408_03865_b200 as pm
+import workload
+from tests._common import TOL, layout, rel_err, to_np
+
+pytestmark = pytest.mark.gpu
+
+DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def problem(R, Dn, L, N, K, kind, io, seed, dev="cuda"):
+    rng = np.random.default_rng(seed)
+    rows = layout(kind, R, L, rng)
+    pos_np, valid = workload.pos_from_rows(rows, L)
+    shape = workload.Shape(f"t{seed}", R, L, Dn, N, K, io)
+    T = workload.row_tensors(torch, shape, list(range(R)), valid, device=dev, dtype=DT[io])
+    P = workload.params(torch, shape, device=dev)
+    pos = torch.as_tensor(pos_np, device=dev)
+    return rows, pos, valid, T, P
+
+
+def run_chain(pos, T, P, silu=True, softplus=True):
+    u = pm.pm_causal_conv1d_fwd(T["x"], P["w"], P["bias"], pos, silu=silu)
+    y, st = pm.pm_selective_scan_fwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
+                                     pos, dt_softplus=softplus)
+    g = pm.pm_selective_scan_bwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos,
+                                 T["dy"], states=st, dt_softplus=softplus)
+    dx, dw, db = pm.pm_causal_conv1d_bwd(T["x"], P["w"], P["bias"], pos, g["du"], silu=silu)
+    torch.cuda.synchronize()
+    return dict(u=u, y=y, states=st, dx=dx, dw=dw, db=db, **g)
+
+
+def check_chain(pos, T, P, out, io, silu=True, softplus=True):
+    """Per-kernel parity of one chained run."""
+    p = to_np(pos).astype(np.int32)
+    x, w, b = to_np(T["x"]), to_np(P["w"]), to_np(P["bias"])
+    A, D, dtb = to_np(P["A"]), to_np(P["D"]), to_np(P["dt_bias"])
+    u_gpu = to_np(out["u"])
+    errs = {}
+    errs["u"] = (rel_err(u_gpu, oracle.conv_fwd(x, w, b, p, silu)), "fwd")
+    args = (u_gpu, to_np(T["dt"]), A, to_np(T["B"]), to_np(T["C"]), D, dtb, p)
+    errs["y"] = (rel_err(to_np(out["y"]), oracle.scan_fwd(*args, softplus=softplus)), "fwd")
+    ref = oracle.scan_bwd(*args, to_np(T["dy"]), softplus=softplus)
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias"):
+        errs[k] = (rel_err(to_np(out[k]), ref[k]), "bwd")
+    rdx, rdw, rdb = oracle.conv_bwd(x, w, b, p, to_np(out["du"]), silu)
+    errs["dx"] = (rel_err(to_np(out["dx"]), rdx), "bwd")
+    errs["dw"] = (rel_err(to_np(out["dw"]), rdw), "bwd")
+    errs["db"] = (rel_err(to_np(out["db"]), rdb), "bwd")
+    bad = {k: (e, TOL[(io, kind)]) for k, (e, kind) in errs.items() if not e <= TOL[(io, kind)]}
+    assert not bad, f"tolerance exceeded: {bad}; all: {errs}"
+    return errs
+
+
+# --------------------------------------------------------------------------
+# the BASELINE tiny config (configs[0]): 1 row L=64 of 20/30/14, Dn 16, N 4
+# --------------------------------------------------------------------------
+
+def test_tiny_config():
+    cfg = workload.CONFIGS["tiny"]
+    pos_np, valid = workload.pos_from_rows(cfg.rows, cfg.L)
+    T = workload.row_tensors(torch, cfg, [0], valid, device="cuda")
+    P = workload.params(torch, cfg, device="cuda")
+    pos = torch.as_tensor(pos_np, device="cuda")
+    out = run_chain(pos, T, P)
+    check_chain(pos, T, P, out, "f32")
+
+
+# --------------------------------------------------------------------------
+# layouts x dtypes x shapes (several tiles/chunks/segments, ragged tails)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+@pytest.mark.parametrize("kind", ["random", "one", "heads", "short", "edges"])
+def test_chain_layouts(io, kind):
+    R, Dn, L, N, K = 3, 200, 1024, 16, 4
+    seed = ["random", "one", "heads", "short", "edges"].index(kind)
+    rows, pos, valid, T, P = problem(R, Dn, L, N, K, kind, io, seed=seed)
+    out = run_chain(pos, T, P)
+    check_chain(pos, T, P, out, io)
+
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+@pytest.mark.parametrize("N,K", [(4, 1), (8, 2), (16, 3), (4, 4)])
+def test_chain_state_and_width(io, N, K):
+    rows, pos, valid, T, P = problem(2, 130, 700, N, K, "random", io, seed=10 * N + K)
+    out = run_chain(pos, T, P)
+    check_chain(pos, T, P, out, io)
+
+
+@pytest.mark.parametrize("L", [1, 7, 13, 100, 1001, 2051])
+def test_ragged_lengths_scalar_path(L):
+    """L not a multiple of 8 takes the scalar (unaligned) path."""
+    rows, pos, valid, T, P = problem(2, 33, L, 16, 4, "random" if L > 3 else "one", "f32",
+                                     seed=L)
+    out = run_chain(pos, T, P)
+    check_chain(pos, T, P, out, "f32")
+
+
+def test_flags_off():
+    rows, pos, valid, T, P = problem(2, 64, 512, 16, 4, "random", "f32", seed=3)
+    T["dt"] = (T["dt"].abs() * 0.1 + 0.01).contiguous()
+    P["dt_bias"] = torch.zeros_like(P["dt_bias"])
+    out = run_chain(pos, T, P, silu=False, softplus=False)
+    check_chain(pos, T, P, out, "f32", silu=False, softplus=False)
+
+
+def test_recompute_states_equals_saved():
+    rows, pos, valid, T, P = problem(2, 96, 900, 16, 4, "random", "f32", seed=4)
+    out = run_chain(pos, T, P)
+    g2 = pm.pm_selective_scan_bwd(out["u"], T["dt"], P["A"], T["B"], T["C"], P["D"],
+                                  P["dt_bias"], pos, T["dy"], states=None)
+    torch.cuda.synchronize()
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias"):
+        assert torch.equal(g2[k], out[k]), k
+
+
+def test_determinism():
+    rows, pos, valid, T, P = problem(2, 256, 1024, 16, 4, "random", "bf16", seed=5)
+    a = run_chain(pos, T, P)
+    b = run_chain(pos, T, P)
+    for k in ("u", "y", "du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dx", "dw", "db"):
+        assert torch.equal(a[k], b[k]), k
+
+
+# --------------------------------------------------------------------------
+# P6: integer-exact regime -> bit-exact (A = 0, delta = 1, small integers)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+def test_integer_exact_bit_exact(io):
+    rng = np.random.default_rng(6)
+    R, Dn, L, N, K = 2, 40, 256, 16, 4
+    rows = layout("short", R, L, rng)
+    pos_np, valid = workload.pos_from_rows(rows, L)
+    pos = torch.as_tensor(pos_np, device="cuda")
+    dt_ = DT[io]
+    ri = lambda lo, hi, shp: torch.as_tensor(rng.integers(lo, hi, shp), device="cuda")
+    x = ri(-2, 3, (R, Dn, L)).to(dt_)
+    w = ri(-1, 2, (Dn, K)).float()
+    bias = ri(-1, 2, (Dn,)).float()
+    u = pm.pm_causal_conv1d_fwd(x, w, bias, pos, silu=False)
+    ref_u = oracle.conv_fwd(to_np(x), to_np(w), to_np(bias), pos_np, silu=False)
+    assert np.array_equal(to_np(u), ref_u)
+    # scan with A = 0 -> abar = ex2(0) = 1 exactly; delta = dt = 1
+    uu = ri(-2, 3, (R, Dn, L)).to(dt_)
+    B = ri(-1, 2, (R, N, L)).to(dt_)
+    C = ri(-1, 2, (R, N, L)).to(dt_)
+    dt = torch.ones((R, Dn, L), device="cuda", dtype=dt_)
+    A = torch.zeros((Dn, N), device="cuda")
+    D = ri(-1, 2, (Dn,)).float()
+    y, st = pm.pm_selective_scan_fwd(uu, dt, A, B, C, D, None, pos, dt_softplus=False)
+    args = (to_np(uu), to_np(dt), to_np(A), to_np(B), to_np(C), to_np(D), None, pos_np)
+    ry = oracle.scan_fwd(*args, softplus=False)
+    if io == "f32" or np.abs(ry).max() <= 256:
+        assert np.array_equal(to_np(y), ry)
+    if io == "f32":
+        dy = ri(-1, 2, (R, Dn, L)).float() * torch.as_tensor(valid, device="cuda")
+        g = pm.pm_selective_scan_bwd(uu, dt, A, B, C, D, None, pos, dy, states=st,
+                                     dt_softplus=False)
+        rg = oracle.scan_bwd(*args, to_np(dy), softplus=False)
+        for k in ("du", "ddt", "dA", "dB", "dC", "dD"):
+            assert np.array_equal(to_np(g[k]), rg[k]), k
+        dx, dw, db = pm.pm_causal_conv1d_bwd(x.float(), w, bias, pos, dy, silu=False)
+        rdx, rdw, rdb = oracle.conv_bwd(to_np(x), to_np(w), to_np(bias), pos_np, to_np(dy),
+                                        silu=False)
+        assert np.array_equal(to_np(dx), rdx)
+        assert np.array_equal(to_np(dw), rdw) and np.array_equal(to_np(db), rdb)
+
+
+# --------------------------------------------------------------------------
+# P2 on the GPU: perturbing one sequence leaves all others bit-identical
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+def test_isolation_gpu(io):
+    R, Dn, L, N, K = 1, 160, 640, 16, 4
+    rows = [[100, 1, 33, 250, 17, 200]]  # 601 slots + 39 padding
+    pos_np, valid = workload.pos_from_rows(rows, L)
+    shape = workload.Shape("iso", R, L, Dn, N, K, io)
+    T = workload.row_tensors(torch, shape, [0], valid, device="cuda", dtype=DT[io])
+    P = workload.params(torch, shape, device="cuda")
+    pos = torch.as_tensor(pos_np, device="cuda")
+    base = run_chain(pos, T, P)
+    j0, j1 = 134, 384  # the 4th sequence
+    T2 = {k: v.clone() for k, v in T.items()}
+    g = torch.Generator(device="cuda").manual_seed(9)
+    for k in ("x", "dt", "dy", "B", "C"):
+        sl = T2[k][:, :, j0:j1]
+        sl.add_((3 * torch.randn(sl.shape, device="cuda", generator=g)).to(sl.dtype))
+    pert = run_chain(pos, T2, P)
+    other = torch.ones(L, dtype=torch.bool, device="cuda")
+    other[j0:j1] = False
+    for k in ("u", "y", "du", "ddt", "dB", "dC", "dx"):
+        assert torch.equal(base[k][..., other], pert[k][..., other]), k
+        assert not torch.equal(base[k][..., j0:j1], pert[k][..., j0:j1]), k
+
+
+# --------------------------------------------------------------------------
+# pm_pack: bit-exact vs the oracle
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("rec", [1, 4, 6, 16, 64])
+def test_pack_bit_exact(rec):
+    rng = np.random.default_rng(rec)
+    lens = workload.gen_lengths(3000, rec)
+    cap = 4096
+    src = rng.integers(0, 256, (int(lens.sum()), rec), dtype=np.uint8)
+    ref_dst, ref_pos = oracle.pack(lens, cap, src)
+    dst, pos, row, off = pm.pm_pack(lens, cap, torch.as_tensor(src, device="cuda"))
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.cpu().numpy(), ref_dst)
+    assert np.array_equal(pos.cpu().numpy(), ref_pos)
+    r2, o2, n2 = oracle.plan_fifo(lens, cap)
+    assert np.array_equal(row, r2) and np.array_equal(off, o2)
+
+
+def test_pack_planned_greedy_bit_exact():
+    rng = np.random.default_rng(1)
+    lens = workload.gen_lengths(2000, 7)
+    cap = 4096
+    src = rng.integers(0, 2**31, int(lens.sum()), dtype=np.int32)
+    row, off, nr = pm.pm_plan_greedy(lens, cap)
+    dst = torch.empty((nr, cap), dtype=torch.int32, device="cuda")
+    pos = torch.empty((nr, cap), dtype=torch.int32, device="cuda")
+    pm.pm_pack_planned(lens, cap, row, off, nr, torch.as_tensor(src, device="cuda"), dst, pos)
+    rr, ro, rn = oracle.plan_ffd(lens, cap)
+    ref_dst, ref_pos = oracle.pack(lens, cap, src.view(np.uint8).reshape(-1, 4), rr, ro)
+    torch.cuda.synchronize()
+    assert np.array_equal(dst.cpu().numpy().view(np.uint8).reshape(nr, cap, 4), ref_dst)
+    assert np.array_equal(pos.cpu().numpy(), ref_pos)
