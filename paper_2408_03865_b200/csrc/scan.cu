@@ -88,6 +88,34 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
   }
 }
 
+template <typename T, bool kVec>
+struct Raw8 {  // 8 consecutive I/O elements held raw in registers (prefetch)
+  float v[8];
+  PM_DEV void load(const T* p, int64_t i, int64_t n) { load8<T, kVec>(p, i, n, v); }
+  PM_DEV void unpack(float (&o)[8]) const {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = v[k];
+  }
+};
+template <>
+struct Raw8<__nv_bfloat16, true> {
+  // kVec guarantees L % 8 == 0, so an 8-aligned vector is either fully inside
+  // the row or fully outside it (then it reads as zeros).
+  uint4 q;
+  PM_DEV void load(const __nv_bfloat16* p, int64_t i, int64_t n) {
+    q = (i >= 0 && i + 8 <= n) ? __ldg(reinterpret_cast<const uint4*>(p + i)) : make_uint4(0, 0, 0, 0);
+  }
+  PM_DEV void unpack(float (&o)[8]) const {
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 x = __bfloat1622float2(b[k]);
+      o[2 * k] = x.x;
+      o[2 * k + 1] = x.y;
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
@@ -127,79 +155,119 @@ scan_fwd_kernel(const ScanFwdArgs a) {
 #pragma unroll
   for (int n = 0; n < N; ++n) h[n] = 0.f;
 
-  for (int j0 = s0 & ~(kTile - 1); j0 < s1; j0 += kTile) {
-    __syncthreads();
-    stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sHead);
-    __syncthreads();
-    const int t_lo = max(s0, j0), t_hi = min(s1, j0 + kTile);
-    for (int sb = (t_lo - j0) & ~7; sb < t_hi - j0; sb += 8) {
-      const int tb = j0 + sb;
-      float uu[8], vv[8], yy[8];
-      load8<T, kVec>(u_row, tb, L, uu);
-      load8<T, kVec>(dt_row, tb, L, vv);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int t = tb + i;
-        yy[i] = 0.f;
-        if (t < t_lo || t >= t_hi) continue;  // CTA-uniform
-        if (a.states != nullptr && (t % kChunk) == 0 && active) {
-          float* st = a.states + (((int64_t)r * a.nchunk + t / kChunk) * N) * Dn + d;
-#pragma unroll
-          for (int n = 0; n < N; ++n) st[(int64_t)n * Dn] = h[n];
-        }
-        const float v = vv[i] + bias;
-        const float delta = a.softplus ? softplusf(v) : v;
-        const float dux = delta * uu[i];
-        float yv = Dd * uu[i];
-        const float* Bt = sB[sb + i];
-        const float* Ct = sC[sb + i];
-        if (sHead[sb + i]) {
-#pragma unroll
-          for (int n = 0; n < N; ++n) h[n] = dux * Bt[n];
-        } else {
-#pragma unroll
-          for (int n = 0; n < N; ++n) h[n] = fmaf(ex2(delta * A2[n]), h[n], dux * Bt[n]);
-        }
-#pragma unroll
-        for (int n = 0; n < N; ++n) yv = fmaf(Ct[n], h[n], yv);
-        yy[i] = yv;
-      }
-      if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, t_lo, t_hi, yy);
+  // Flat loop over 8-step sub-blocks; u/dt of the next sub-block are loaded
+  // into registers before the current one is computed (software pipeline),
+  // B/C/head tiles are restaged at every kTile boundary.
+  int tb = s0 & ~7;
+  Raw8<T, kVec> pu, pt;
+  pu.load(u_row, tb, L);
+  pt.load(dt_row, tb, L);
+  int j0 = -1;
+  for (; tb < s1; tb += 8) {
+    if (j0 < 0 || (tb & (kTile - 1)) == 0) {  // CTA-uniform
+      j0 = tb & ~(kTile - 1);
+      __syncthreads();
+      stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sHead);
+      __syncthreads();
     }
+    float uu[8], vv[8], yy[8];
+    pu.unpack(uu);
+    pt.unpack(vv);
+    if (tb + 8 < s1) {
+      pu.load(u_row, tb + 8, L);
+      pt.load(dt_row, tb + 8, L);
+    }
+    const int sb = tb - j0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int t = tb + i;
+      yy[i] = 0.f;
+      if (t < s0 || t >= s1) continue;  // CTA-uniform
+      if (a.states != nullptr && (t % kChunk) == 0 && active) {
+        float* st = a.states + (((int64_t)r * a.nchunk + t / kChunk) * N) * Dn + d;
+#pragma unroll
+        for (int n = 0; n < N; ++n) st[(int64_t)n * Dn] = h[n];
+      }
+      const float v = vv[i] + bias;
+      const float delta = a.softplus ? softplusf(v) : v;
+      const float dux = delta * uu[i];
+      float yv = Dd * uu[i];
+      const float* Bt = sB[sb + i];
+      const float* Ct = sC[sb + i];
+      if (sHead[sb + i]) {
+#pragma unroll
+        for (int n = 0; n < N; ++n) h[n] = dux * Bt[n];
+      } else {
+#pragma unroll
+        for (int n = 0; n < N; ++n) h[n] = fmaf(ex2(delta * A2[n]), h[n], dux * Bt[n]);
+      }
+#pragma unroll
+      for (int n = 0; n < N; ++n) yv = fmaf(Ct[n], h[n], yv);
+      yy[i] = yv;
+    }
+    if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
   }
 }
 
 // ---------------------------------------------------------------------------
 // backward
 // ---------------------------------------------------------------------------
+// Layout: a CTA owns kBwdCh channels of one row and one time segment; each
+// channel is served by a lane pair (lane = 2*c + hf), thread hf holding the
+// NH = N/2 states [hf*NH, hf*NH + NH) -- half the registers of a
+// one-thread-per-channel design, so 12 warps fit per SM.
+// Per chunk of kChunk steps (walked in reverse):
+//   phase 1: per-(t,d) scalars delta, u, dy, sigmoid(v) computed ONCE into
+//            shared memory from registers prefetched during the previous
+//            chunk; B/C/head staged as fp32;
+//   pass A : forward recompute from the saved chunk state, storing the state
+//            at every kSub-step sub-chunk start (shared memory);
+//   pass B : per sub-chunk (reverse): recompute h_t, abar_t into registers,
+//            then the reverse recurrence g_t = C_t dy_t + abar_{t+1} g_{t+1}
+//            (abar = 0 at heads); sum_n terms are combined across the
+//            lane pair with one shuffle; dB/dC values are reduced over the
+//            CTA's channels in 2-step rounds (warp transpose through a
+//            conflict-free padded buffer, then across warps).
+constexpr int kBwdCh = 64;                   // channels per CTA
+constexpr int kBwdThreads = 2 * kBwdCh;      // lane pair per channel
+constexpr int kBwdWarps = kBwdThreads / 32;
+constexpr int kRedStride = 36;               // float4 per transpose row (== 4 mod 8)
+static_assert(kChunk == 16, "phase 1 maps 8 steps to each thread of a pair");
+
 template <int N>
 struct BwdSmem {
-  static constexpr int kQ = (2 * N) / 4;          // float4 quads of (dB, dC) values
-  static constexpr int kRows = kSub * kQ;         // transpose rows per warp
-  float4 sub[kNSub][N / 4][kScanThreads];         // sub-chunk start states
-  float4 red[kScanWarps][kRows][33];              // warp transpose (padded)
-  float4 xw[2][kScanWarps][32];                   // cross-warp partials
+  static constexpr int NH = N / 2;   // states per thread
+  static constexpr int kQ = N / 4;   // float4 quads of (dB, dC) values per thread-step
+  static constexpr int kRows = 2 * kQ;  // transpose rows per 2-step round
+  float sd[kChunk][kBwdCh];   // delta
+  float su[kChunk][kBwdCh];   // u (0 on inactive channels)
+  float sy[kChunk][kBwdCh];   // dy (0 on inactive channels)
+  float ss[kChunk][kBwdCh];   // softplus'(v) (1 if softplus off)
+  float2 sub[kNSub][NH / 2][kBwdThreads];  // sub-chunk start states
+  float4 red[kBwdWarps][kRows][kRedStride];
+  float4 xw[2][kBwdWarps][kRows][2];
   float B[kChunk][N];
   float C[kChunk][N];
   int head[kChunk];
-  int s_red[kScanWarps];
+  int s_red[kBwdWarps];
 };
 
 template <typename T, int N, bool kVec>
-__global__ void __launch_bounds__(kScanThreads, 2)
+__global__ void __launch_bounds__(kBwdThreads, 3)
 scan_bwd_kernel(const ScanBwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using SM = BwdSmem<N>;
+  constexpr int NH = SM::NH, kQ = SM::kQ, kRows = SM::kRows;
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
-  constexpr int kQ = SM::kQ;
-  static_assert(kQ <= 8 && SM::kRows <= 32, "transpose rows must fit a warp");
 
   const int r = blockIdx.y, k = blockIdx.z, dblk = blockIdx.x;
   const int L = a.L, Dn = a.Dn;
-  const int lid = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int d_raw = dblk * kScanThreads + threadIdx.x;
+  const int tid = threadIdx.x, lid = tid & 31, wid = tid >> 5;
+  const int cl = tid >> 1, hf = tid & 1;
+  const int d_raw = dblk * kBwdCh + cl;
   const bool active = d_raw < Dn;
   const int d = active ? d_raw : Dn - 1;
+  const int n0 = hf * NH;  // first state of this thread
   const int32_t* pos_row = a.pos + (int64_t)r * L;
   float* wsp = a.ws_param + (int64_t)(r * a.nseg + k) * (N + 2) * Dn;
 
@@ -207,7 +275,12 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   segment_bounds(pos_row, L, k, a.nseg, sm.s_red, s0, s1);
   if (s0 >= s1) {
     if (active) {
-      for (int n = 0; n < N + 2; ++n) wsp[(int64_t)n * Dn + d] = 0.f;
+#pragma unroll
+      for (int j = 0; j < NH; ++j) wsp[(int64_t)(n0 + j) * Dn + d] = 0.f;
+      if (hf == 0) {
+        wsp[(int64_t)N * Dn + d] = 0.f;
+        wsp[(int64_t)(N + 1) * Dn + d] = 0.f;
+      }
     }
     return;
   }
@@ -222,12 +295,12 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   T* ddt_row = static_cast<T*>(a.ddt) + lane;
   float* ws_bc_r = a.ws_bc + ((int64_t)dblk * a.R + r) * (int64_t)L * (2 * N);
 
-  float A2[N], g[N], dA[N];
+  float A2[NH], g[NH], dA[NH];
 #pragma unroll
-  for (int n = 0; n < N; ++n) {
-    A2[n] = __ldg(a.A + (int64_t)d * N + n) * kLog2e;
-    g[n] = 0.f;
-    dA[n] = 0.f;
+  for (int j = 0; j < NH; ++j) {
+    A2[j] = __ldg(a.A + (int64_t)d * N + n0 + j) * kLog2e;
+    g[j] = 0.f;
+    dA[j] = 0.f;
   }
   const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
   const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
@@ -235,50 +308,77 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   int xbuf = 0;
 
   const int cfirst = s0 / kChunk, clast = (s1 - 1) / kChunk;
+  Raw8<T, kVec> pu, pt, py;  // prefetched raw rows: steps [cb + 8hf, +8)
+  {
+    const int64_t i0 = (int64_t)clast * kChunk + 8 * hf;
+    pu.load(u_row, i0, L);
+    pt.load(dt_row, i0, L);
+    py.load(dy_row, i0, L);
+  }
+
   for (int c = clast; c >= cfirst; --c) {
     const int cb = c * kChunk, c0 = max(cb, s0), c1 = min(cb + kChunk, s1);
-    __syncthreads();
-    stage_bc<T, N, kChunk, kVec>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.head);
-    // chunk start state (state before step cb); irrelevant when cb <= s0
-    // because s0 is a head.
-    float h[N];
+    // chunk start state (irrelevant when cb <= s0: s0 is a head)
+    float h[NH];
     if (cb > s0) {
-      const float* st = a.states + (((int64_t)r * a.nchunk + c) * N) * Dn + d;
+      const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
 #pragma unroll
-      for (int n = 0; n < N; ++n) h[n] = st[(int64_t)n * Dn];
+      for (int j = 0; j < NH; ++j) h[j] = st[(int64_t)j * Dn];
     } else {
 #pragma unroll
-      for (int n = 0; n < N; ++n) h[n] = 0.f;
+      for (int j = 0; j < NH; ++j) h[j] = 0.f;
     }
+    __syncthreads();  // previous chunk's readers of sd/su/sy/ss/B/C are done
+    // ---- phase 1: per-(t,d) scalars for steps [cb + 8hf, +8) ----
+    {
+      float uu[8], vv[8], yy[8];
+      pu.unpack(uu);
+      pt.unpack(vv);
+      py.unpack(yy);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int ii = 8 * hf + i;
+        const float v = vv[i] + bias;
+        float dl = v, sg = 1.f;
+        if (a.softplus) {
+          const float e = ex2(v * kLog2e);
+          dl = v > 20.f ? v : log1pf(e);
+          sg = v > 20.f ? 1.f : __fdividef(e, 1.f + e);
+        }
+        sm.sd[ii][cl] = dl;
+        sm.su[ii][cl] = active ? uu[i] : 0.f;
+        sm.sy[ii][cl] = active ? yy[i] : 0.f;
+        sm.ss[ii][cl] = sg;
+      }
+    }
+    stage_bc<T, N, kChunk, kVec>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.head);
     __syncthreads();
+    if (c > cfirst) {  // prefetch the next (earlier) chunk while this one computes
+      const int64_t i0 = (int64_t)(c - 1) * kChunk + 8 * hf;
+      pu.load(u_row, i0, L);
+      pt.load(dt_row, i0, L);
+      py.load(dy_row, i0, L);
+    }
 
     // ---- pass A: forward over the chunk, record sub-chunk start states ----
 #pragma unroll
-    for (int sb = 0; sb < kChunk; sb += 8) {
-      float uu[8], vv[8];
-      load8<T, kVec>(u_row, cb + sb, L, uu);
-      load8<T, kVec>(dt_row, cb + sb, L, vv);
+    for (int ii = 0; ii < kChunk; ++ii) {
+      const int t = cb + ii;
+      if (ii % kSub == 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int ii = sb + i, t = cb + ii;
-        if (ii % kSub == 0) {
+        for (int q = 0; q < NH / 2; ++q)
+          sm.sub[ii / kSub][q][tid] = make_float2(h[2 * q], h[2 * q + 1]);
+      }
+      if (t < c0 || t >= c1) continue;  // CTA-uniform
+      const float delta = sm.sd[ii][cl];
+      const float dux = delta * sm.su[ii][cl];
+      const float* Bt = &sm.B[ii][n0];
+      if (sm.head[ii]) {
 #pragma unroll
-          for (int q = 0; q < N / 4; ++q)
-            sm.sub[ii / kSub][q][threadIdx.x] =
-                make_float4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
-        }
-        if (t < c0 || t >= c1) continue;
-        const float v = vv[i] + bias;
-        const float delta = a.softplus ? softplusf(v) : v;
-        const float dux = delta * uu[i];
-        const float* Bt = sm.B[ii];
-        if (sm.head[ii]) {
+        for (int j = 0; j < NH; ++j) h[j] = dux * Bt[j];
+      } else {
 #pragma unroll
-          for (int n = 0; n < N; ++n) h[n] = dux * Bt[n];
-        } else {
-#pragma unroll
-          for (int n = 0; n < N; ++n) h[n] = fmaf(ex2(delta * A2[n]), h[n], dux * Bt[n]);
-        }
+        for (int j = 0; j < NH; ++j) h[j] = fmaf(ex2(delta * A2[j]), h[j], dux * Bt[j]);
       }
     }
 
@@ -286,132 +386,139 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     for (int sc = kNSub - 1; sc >= 0; --sc) {
       const int a0 = cb + sc * kSub;
       if (a0 >= c1 || a0 + kSub <= c0) continue;  // CTA-uniform
-      float uu[4], vv[4], yy[4];
-      load4<T, kVec>(u_row, a0, L, uu);
-      load4<T, kVec>(dt_row, a0, L, vv);
-      load4<T, kVec>(dy_row, a0, L, yy);
-      float dl[4], sg[4];
+      float hb[kSub][NH], ab[kSub][NH];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float v = vv[i] + bias;
-        if (a.softplus) {
-          dl[i] = softplusf(v);
-          sg[i] = sigmoidf_fast(v);
-        } else {
-          dl[i] = v;
-          sg[i] = 1.f;
-        }
-      }
-      // recompute h_t and abar_t for the sub-chunk into registers
-      float hb[kSub][N], ab[kSub][N];
-#pragma unroll
-      for (int q = 0; q < N / 4; ++q) {
-        const float4 s = sm.sub[sc][q][threadIdx.x];
-        h[4 * q] = s.x; h[4 * q + 1] = s.y; h[4 * q + 2] = s.z; h[4 * q + 3] = s.w;
+      for (int q = 0; q < NH / 2; ++q) {
+        const float2 s2 = sm.sub[sc][q][tid];
+        h[2 * q] = s2.x;
+        h[2 * q + 1] = s2.y;
       }
 #pragma unroll
       for (int i = 0; i < kSub; ++i) {
         const int t = a0 + i, ii = t - cb;
-        const bool valid = t >= c0 && t < c1;
-        const float dux = dl[i] * uu[i];
-        const float* Bt = sm.B[ii];
-        const bool head = sm.head[ii];
+        if (t >= c0 && t < c1) {  // CTA-uniform
+          const float delta = sm.sd[ii][cl];
+          const float dux = delta * sm.su[ii][cl];
+          const float* Bt = &sm.B[ii][n0];
+          if (sm.head[ii]) {
 #pragma unroll
-        for (int n = 0; n < N; ++n) {
-          float ab_ = head ? 0.f : ex2(dl[i] * A2[n]);
-          float hn = head ? dux * Bt[n] : fmaf(ab_, h[n], dux * Bt[n]);
-          if (!valid) { ab_ = 0.f; hn = h[n]; }
-          ab[i][n] = ab_;
-          hb[i][n] = hn;
-          h[n] = hn;
-        }
-      }
-      // reverse recurrence over the sub-chunk
-      float duo[4], ddo[4];
+            for (int j = 0; j < NH; ++j) {
+              ab[i][j] = 0.f;
+              h[j] = dux * Bt[j];
+            }
+          } else {
 #pragma unroll
-      for (int i = kSub - 1; i >= 0; --i) {
-        const int t = a0 + i, ii = t - cb;
-        const bool valid = t >= c0 && t < c1;  // CTA-uniform
-        float4* rrow = &sm.red[wid][i * kQ][lid];
-        if (!valid) {
-#pragma unroll
-          for (int q = 0; q < kQ; ++q) rrow[q * 33] = make_float4(0.f, 0.f, 0.f, 0.f);
-          duo[i] = 0.f;
-          ddo[i] = 0.f;
-          continue;
-        }
-        const float dyv = yy[i], ux = uu[i], delta = dl[i];
-        const float dux = delta * ux;
-        const bool head = sm.head[ii];
-        const float* Bt = sm.B[ii];
-        const float* Ct = sm.C[ii];
-        float Ssum = 0.f, dq = 0.f;
-#pragma unroll
-        for (int q4 = 0; q4 < N / 4; ++q4) {
-          float vb[4], vc[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int n = 4 * q4 + j;
-            g[n] = fmaf(Ct[n], dyv, g[n]);  // g holds abar_{t+1} g_{t+1}
-            Ssum = fmaf(g[n], Bt[n], Ssum);
-            const float hm = head ? 0.f : fmaf(-dux, Bt[n], hb[i][n]);  // abar_t h_{t-1}
-            const float q = g[n] * hm;
-            dA[n] = fmaf(delta, q, dA[n]);
-            dq = fmaf(A2[n], q, dq);
-            vb[j] = g[n] * dux;
-            vc[j] = dyv * hb[i][n];
-            g[n] = ab[i][n] * g[n];  // carry to t-1 (0 at heads)
+            for (int j = 0; j < NH; ++j) {
+              ab[i][j] = ex2(delta * A2[j]);
+              h[j] = fmaf(ab[i][j], h[j], dux * Bt[j]);
+            }
           }
-          rrow[q4 * 33] = make_float4(vb[0], vb[1], vb[2], vb[3]);
-          rrow[(N / 4 + q4) * 33] = make_float4(vc[0], vc[1], vc[2], vc[3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NH; ++j) ab[i][j] = 0.f;
         }
-        duo[i] = fmaf(Dd, dyv, delta * Ssum);
-        const float dd = fmaf(ux, Ssum, dq * kLn2);
-        ddo[i] = dd * sg[i];
-        dD = fmaf(dyv, ux, dD);
-        ddtb += ddo[i];
+#pragma unroll
+        for (int j = 0; j < NH; ++j) hb[i][j] = h[j];
       }
-      if (active) {
+      float duo[kSub], ddo[kSub];
+#pragma unroll
+      for (int round = kSub / 2 - 1; round >= 0; --round) {
+#pragma unroll
+        for (int s = 1; s >= 0; --s) {
+          const int i = 2 * round + s;
+          const int t = a0 + i, ii = t - cb;
+          float4* rrow = &sm.red[wid][s * kQ][lid];
+          if (t < c0 || t >= c1) {  // CTA-uniform
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) rrow[q * kRedStride] = make_float4(0.f, 0.f, 0.f, 0.f);
+            duo[i] = 0.f;
+            ddo[i] = 0.f;
+            continue;
+          }
+          const float delta = sm.sd[ii][cl], ux = sm.su[ii][cl], dyv = sm.sy[ii][cl];
+          const float dux = delta * ux;
+          const bool head = sm.head[ii];
+          const float* Bt = &sm.B[ii][n0];
+          const float* Ct = &sm.C[ii][n0];
+          float Ssum = 0.f, dq = 0.f;
+          float vals[N];  // [dB of my NH states | dC of my NH states]
+#pragma unroll
+          for (int j = 0; j < NH; ++j) {
+            g[j] = fmaf(Ct[j], dyv, g[j]);  // g holds abar_{t+1} g_{t+1}
+            Ssum = fmaf(g[j], Bt[j], Ssum);
+            const float hm = head ? 0.f : fmaf(-dux, Bt[j], hb[i][j]);  // abar_t h_{t-1}
+            const float q = g[j] * hm;
+            dA[j] = fmaf(delta, q, dA[j]);
+            dq = fmaf(A2[j], q, dq);
+            vals[j] = g[j] * dux;
+            vals[NH + j] = dyv * hb[i][j];
+            g[j] = ab[i][j] * g[j];  // carry to t-1 (0 at heads)
+          }
+#pragma unroll
+          for (int q = 0; q < kQ; ++q)
+            rrow[q * kRedStride] = make_float4(vals[4 * q], vals[4 * q + 1], vals[4 * q + 2], vals[4 * q + 3]);
+          Ssum += __shfl_xor_sync(0xffffffffu, Ssum, 1);
+          dq += __shfl_xor_sync(0xffffffffu, dq, 1);
+          duo[i] = fmaf(Dd, dyv, delta * Ssum);
+          ddo[i] = fmaf(ux, Ssum, dq * kLn2) * sm.ss[ii][cl];
+          dD = fmaf(dyv, ux, dD);
+          ddtb += ddo[i];
+        }
+        // warp transpose-reduce of the round: lane -> (row, half, column half)
+        __syncwarp();
+        {
+          const int row = lid >> 2, rh = lid & 1, ch = (lid >> 1) & 1;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row < kRows) {
+            const float4* rp = &sm.red[wid][row][2 * ch + rh];
+            float4 p0 = rp[0], p1 = rp[4], p2 = rp[8], p3 = rp[12];
+            float4 p4 = rp[16], p5 = rp[20], p6 = rp[24], p7 = rp[28];
+            acc.x = ((p0.x + p1.x) + (p2.x + p3.x)) + ((p4.x + p5.x) + (p6.x + p7.x));
+            acc.y = ((p0.y + p1.y) + (p2.y + p3.y)) + ((p4.y + p5.y) + (p6.y + p7.y));
+            acc.z = ((p0.z + p1.z) + (p2.z + p3.z)) + ((p4.z + p5.z) + (p6.z + p7.z));
+            acc.w = ((p0.w + p1.w) + (p2.w + p3.w)) + ((p4.w + p5.w) + (p6.w + p7.w));
+          }
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+          acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
+          acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 2);
+          if (row < kRows && ch == 0) sm.xw[xbuf][wid][row][rh] = acc;
+        }
+        __syncthreads();
+        // cross-warp sum: 2 steps x 2N values
+        for (int e = tid; e < 2 * 2 * N; e += kBwdThreads) {
+          const int s = e / (2 * N), v = e % (2 * N);
+          const int t = a0 + 2 * round + s;
+          if (t >= c0 && t < c1) {
+            const int n = v < N ? v : v - N;
+            const int rh = n / NH;
+            const int kk = (v < N ? 0 : NH) + n % NH;
+            const int row = s * kQ + kk / 4, comp = kk % 4;
+            float acc = 0.f;
+#pragma unroll
+            for (int w = 0; w < kBwdWarps; ++w) {
+              const float4 p = sm.xw[xbuf][w][row][rh];
+              acc += comp == 0 ? p.x : comp == 1 ? p.y : comp == 2 ? p.z : p.w;
+            }
+            ws_bc_r[(int64_t)t * (2 * N) + v] = acc;
+          }
+        }
+        xbuf ^= 1;
+        __syncwarp();
+      }
+      if (active && hf == 0) {
         store4<T, kVec>(du_row, a0, c0, c1, duo);
         store4<T, kVec>(ddt_row, a0, c0, c1, ddo);
       }
-      // warp transpose-reduce: lane j owns row j = (step i, quad q)
-      __syncwarp();
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (lid < SM::kRows) {
-        const float4* row = sm.red[wid][lid];
-#pragma unroll 8
-        for (int l = 0; l < 32; ++l) {
-          const float4 v = row[l];
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
-      }
-      sm.xw[xbuf][wid][lid] = acc;
-      __syncthreads();
-      // cross-warp sum; thread -> (step i, value v) ; 2N values per step
-      for (int e = threadIdx.x; e < kSub * 2 * N; e += kScanThreads) {
-        const int i = e / (2 * N), v = e % (2 * N);
-        const int t = a0 + i;
-        if (t >= c0 && t < c1) {
-          const int row = i * kQ + v / 4, comp = v % 4;
-          float s = 0.f;
-#pragma unroll
-          for (int w = 0; w < kScanWarps; ++w) {
-            const float4 p = sm.xw[xbuf][w][row];
-            s += comp == 0 ? p.x : comp == 1 ? p.y : comp == 2 ? p.z : p.w;
-          }
-          ws_bc_r[(int64_t)t * (2 * N) + v] = s;
-        }
-      }
-      xbuf ^= 1;
-      __syncwarp();
     }
   }
   if (active) {
 #pragma unroll
-    for (int n = 0; n < N; ++n) wsp[(int64_t)n * Dn + d] = dA[n];
-    wsp[(int64_t)N * Dn + d] = dD;
-    wsp[(int64_t)(N + 1) * Dn + d] = ddtb;
+    for (int j = 0; j < NH; ++j) wsp[(int64_t)(n0 + j) * Dn + d] = dA[j];
+    if (hf == 0) {
+      wsp[(int64_t)N * Dn + d] = dD;
+      wsp[(int64_t)(N + 1) * Dn + d] = ddtb;
+    }
   }
 }
 
@@ -467,17 +574,20 @@ using namespace pm;
 
 int n_chunks(int64_t L) { return (int)((L + kChunk - 1) / kChunk); }
 int n_dblk(int64_t Dn) { return (int)((Dn + kScanThreads - 1) / kScanThreads); }
+int n_dblk_bwd(int64_t Dn) { return (int)((Dn + kBwdCh - 1) / kBwdCh); }
 
-// Segments per row: enough CTAs for ~4 resident waves on 148 SMs, but keep
-// nominal segments >= 256 steps (actual cuts snap to heads anyway).
-int n_segments(int64_t R, int64_t Dn, int64_t L) {
-  const int64_t ctas = R * n_dblk(Dn);
-  const int64_t target = 4 * 148 * 2;
+// Segments per row: enough CTAs for ~4 waves of the kernel's resident CTAs
+// on 148 SMs, but keep nominal segments >= 256 steps (cuts snap to heads).
+int n_segments(int64_t R, int64_t nblk, int64_t L, int64_t resident_per_sm) {
+  const int64_t ctas = R * nblk;
+  const int64_t target = 4 * 148 * resident_per_sm;
   int64_t s = (target + ctas - 1) / ctas;
   s = std::min<int64_t>(s, std::max<int64_t>(1, L / 256));
   s = std::max<int64_t>(s, 1);
   return (int)std::min<int64_t>(s, 64);
 }
+int nseg_fwd(int64_t R, int64_t Dn, int64_t L) { return n_segments(R, n_dblk(Dn), L, 6); }
+int nseg_bwd(int64_t R, int64_t Dn, int64_t L) { return n_segments(R, n_dblk_bwd(Dn), L, 3); }
 
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -524,11 +634,11 @@ pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, floa
   auto kern = scan_bwd_kernel<T, N, kVec>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return PM_ERR_CUDA;
-  dim3 grid(n_dblk(a.Dn), a.R, a.nseg);
-  kern<<<grid, kScanThreads, smem, s>>>(a);
+  dim3 grid(n_dblk_bwd(a.Dn), a.R, a.nseg);
+  kern<<<grid, kBwdThreads, smem, s>>>(a);
   PM_LAUNCH_CHECK();
   dim3 g2((a.L + 31) / 32, a.R);
-  scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk(a.Dn), a.R, a.L);
+  scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
   PM_LAUNCH_CHECK();
   const int64_t np = (int64_t)(N + 2) * a.Dn;
   scan_bwd_finalize_param<N><<<(unsigned)((np + 255) / 256), 256, 0, s>>>(
@@ -559,8 +669,8 @@ size_t state_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
 }
 
 size_t bwd_ws_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N, bool recompute) {
-  size_t bc = (size_t)n_dblk(Dn) * R * L * 2 * N * sizeof(float);
-  size_t par = (size_t)R * n_segments(R, Dn, L) * (N + 2) * Dn * sizeof(float);
+  size_t bc = (size_t)n_dblk_bwd(Dn) * R * L * 2 * N * sizeof(float);
+  size_t par = (size_t)R * nseg_bwd(R, Dn, L) * (N + 2) * Dn * sizeof(float);
   size_t st = recompute ? state_bytes(R, Dn, L, N) : 0;
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   return up(bc) + up(par) + up(st);
@@ -598,7 +708,7 @@ pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, c
   const bool vec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
                    aligned16(C) && aligned16(y);
   ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, y, states,
-                (int)R, (int)Dn, (int)L, n_segments(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
+                (int)R, (int)Dn, (int)L, nseg_fwd(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return io == PM_F32 ? dispatch_fwd<float>(a, N, vec, s) : dispatch_fwd<__nv_bfloat16>(a, N, vec, s);
 }
@@ -630,21 +740,21 @@ pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, c
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   char* w = static_cast<char*>(workspace);
   float* ws_bc = reinterpret_cast<float*>(w);
-  w += up((size_t)n_dblk(Dn) * R * L * 2 * N * sizeof(float));
+  w += up((size_t)n_dblk_bwd(Dn) * R * L * 2 * N * sizeof(float));
   float* ws_par = reinterpret_cast<float*>(w);
-  w += up((size_t)R * n_segments(R, Dn, L) * (N + 2) * Dn * sizeof(float));
+  w += up((size_t)R * nseg_bwd(R, Dn, L) * (N + 2) * Dn * sizeof(float));
   const float* stp = states;
   if (recompute) {
     float* st_ws = reinterpret_cast<float*>(w);
     ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws,
-                   (int)R, (int)Dn, (int)L, n_segments(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
+                   (int)R, (int)Dn, (int)L, nseg_fwd(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
     pm_status fs = io == PM_F32 ? dispatch_fwd<float>(fa, N, vec, s)
                                 : dispatch_fwd<__nv_bfloat16>(fa, N, vec, s);
     if (fs != PM_OK) return fs;
     stp = st_ws;
   }
   ScanBwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, stp, dy, du, ddt, ws_bc, ws_par,
-                (int)R, (int)Dn, (int)L, n_segments(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
+                (int)R, (int)Dn, (int)L, nseg_bwd(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
   return io == PM_F32 ? dispatch_bwd<float>(a, N, vec, dA, dB, dC, dD, ddt_bias, s)
                       : dispatch_bwd<__nv_bfloat16>(a, N, vec, dA, dB, dC, dD, ddt_bias, s);
 }

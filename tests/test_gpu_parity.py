@@ -168,7 +168,7 @@ def test_integer_exact_bit_exact(io):
     if io == "f32" or np.abs(ry).max() <= 256:
         assert np.array_equal(to_np(y), ry)
     if io == "f32":
-        dy = ri(-1, 2, (R, Dn, L)).float() * torch.as_tensor(valid, device="cuda")
+        dy = ri(-1, 2, (R, Dn, L)).float() * torch.as_tensor(valid, device="cuda")[:, None, :]
         g = pm.pm_selective_scan_bwd(uu, dt, A, B, C, D, None, pos, dy, states=st,
                                      dt_softplus=False)
         rg = oracle.scan_bwd(*args, to_np(dy), softplus=False)
