@@ -37,11 +37,13 @@ template <typename T> struct IO;
 template <> struct IO<float> {
   static PM_DEV float ld(const float* p) { return __ldg(p); }
   static PM_DEV void st(float* p, float v) { *p = v; }
+  static PM_DEV float cvt(float v) { return v; }
   static constexpr int kIsz = 4;
 };
 template <> struct IO<__nv_bfloat16> {
   static PM_DEV float ld(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
   static PM_DEV void st(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+  static PM_DEV float cvt(__nv_bfloat16 v) { return __bfloat162float(v); }
   static constexpr int kIsz = 2;
 };
 
@@ -132,6 +134,16 @@ PM_DEV void store4(T* __restrict__ p, int64_t i, int64_t lo, int64_t hi, const f
       if (i + k >= lo && i + k < hi) IO<T>::st(p + i + k, v[k]);
   }
 }
+
+// ------------------------------------------------------------ cp.async ----
+// 16-byte global->shared async copy (LDGSTS); src_bytes < 16 zero-fills.
+PM_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+PM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+PM_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // --------------------------------------------------- segment splitting ----
 // A packed row is a concatenation of independent sequences (no

@@ -217,46 +217,106 @@ scan_fwd_kernel(const ScanFwdArgs a) {
 // NH = N/2 states [hf*NH, hf*NH + NH) -- half the registers of a
 // one-thread-per-channel design, so 12 warps fit per SM.
 // Per chunk of kChunk steps (walked in reverse):
-//   phase 1: per-(t,d) scalars delta, u, dy, sigmoid(v) computed ONCE into
-//            shared memory from registers prefetched during the previous
-//            chunk; B/C/head staged as fp32;
+//   staging: every per-chunk input (u, dt, dy rows, B, C, pos, the saved
+//            chunk state) is fetched with cp.async one chunk AHEAD into a raw
+//            shared buffer, so no global latency sits on the critical path;
+//   phase 1: per-(t,d) scalars delta, u, dy, softplus'(v) computed once into
+//            shared memory; B/C converted to fp32; head flags;
 //   pass A : forward recompute from the saved chunk state, storing the state
 //            at every kSub-step sub-chunk start (shared memory);
 //   pass B : per sub-chunk (reverse): recompute h_t, abar_t into registers,
 //            then the reverse recurrence g_t = C_t dy_t + abar_{t+1} g_{t+1}
 //            (abar = 0 at heads); sum_n terms are combined across the
-//            lane pair with one shuffle; dB/dC values are reduced over the
-//            CTA's channels in 2-step rounds (warp transpose through a
-//            conflict-free padded buffer, then across warps).
+//            lane pair with one shuffle; dB/dC values are reduced over each
+//            warp's channels in 2-step rounds (warp transpose through a
+//            conflict-free padded buffer) and the per-warp partials of the
+//            whole chunk are summed across warps after ONE barrier.
 constexpr int kBwdCh = 64;                   // channels per CTA
 constexpr int kBwdThreads = 2 * kBwdCh;      // lane pair per channel
 constexpr int kBwdWarps = kBwdThreads / 32;
 constexpr int kRedStride = 36;               // float4 per transpose row (== 4 mod 8)
 static_assert(kChunk == 16, "phase 1 maps 8 steps to each thread of a pair");
 
-template <int N>
+template <typename T, int N>
+struct BwdRaw {  // raw inputs of one chunk, filled by cp.async (vector path)
+  T u[kBwdCh][kChunk];
+  T dt[kBwdCh][kChunk];
+  T dy[kBwdCh][kChunk];
+  T B[N][kChunk];
+  T C[N][kChunk];
+  int32_t pos[kChunk];
+  float st[N][kBwdCh];
+};
+
+template <typename T, int N>
 struct BwdSmem {
   static constexpr int NH = N / 2;   // states per thread
   static constexpr int kQ = N / 4;   // float4 quads of (dB, dC) values per thread-step
   static constexpr int kRows = 2 * kQ;  // transpose rows per 2-step round
+  BwdRaw<T, N> raw;
   float sd[kChunk][kBwdCh];   // delta
   float su[kChunk][kBwdCh];   // u (0 on inactive channels)
   float sy[kChunk][kBwdCh];   // dy (0 on inactive channels)
   float ss[kChunk][kBwdCh];   // softplus'(v) (1 if softplus off)
   float2 sub[kNSub][NH / 2][kBwdThreads];  // sub-chunk start states
   float4 red[kBwdWarps][kRows][kRedStride];
-  float4 xw[2][kBwdWarps][kRows][2];
+  float4 xw[kChunk / 2][kBwdWarps][kRows][2];
   float B[kChunk][N];
   float C[kChunk][N];
   int head[kChunk];
   int s_red[kBwdWarps];
 };
 
+// Issue the cp.async copies of chunk c's raw inputs (vector path only:
+// L*isz % 16 == 0, Dn % 4 == 0, 16-byte aligned pointers).
+template <typename T, int N>
+PM_DEV void bwd_issue_raw(BwdRaw<T, N>& rw, const ScanBwdArgs& a, int r, int dblk, int c, int s0) {
+  constexpr int kEl = 16 / (int)sizeof(T);       // elements per 16-byte chunk
+  constexpr int kRowQ = kChunk / kEl;            // chunks per (row, chunk)
+  const int L = a.L, Dn = a.Dn, cb = c * kChunk;
+  const T* srcs[3] = {static_cast<const T*>(a.u), static_cast<const T*>(a.dt),
+                      static_cast<const T*>(a.dy)};
+  T(*dsts[3])[kChunk] = {rw.u, rw.dt, rw.dy};
+  constexpr int kTx = kBwdCh * kRowQ;
+  for (int e = threadIdx.x; e < 3 * kTx; e += kBwdThreads) {
+    const int arr = e / kTx, rem = e % kTx, ch = rem / kRowQ, q = rem % kRowQ;
+    const int d = dblk * kBwdCh + ch;
+    const int t0 = cb + q * kEl;
+    const bool ok = d < Dn && t0 < L;
+    const T* src = ok ? srcs[arr] + ((int64_t)r * Dn + d) * L + t0 : srcs[arr];
+    cp_async16(&dsts[arr][ch][q * kEl], src, ok ? 16 : 0);
+  }
+  const T* Bp = static_cast<const T*>(a.B) + (int64_t)r * N * L;
+  const T* Cp = static_cast<const T*>(a.C) + (int64_t)r * N * L;
+  for (int e = threadIdx.x; e < 2 * N * kRowQ; e += kBwdThreads) {
+    const int arr = e / (N * kRowQ), rem = e % (N * kRowQ), n = rem / kRowQ, q = rem % kRowQ;
+    const int t0 = cb + q * kEl;
+    const bool ok = t0 < L;
+    const T* src = (arr == 0 ? Bp : Cp) + (int64_t)n * L + (ok ? t0 : 0);
+    cp_async16(&(arr == 0 ? rw.B : rw.C)[n][q * kEl], src, ok ? 16 : 0);
+  }
+  for (int e = threadIdx.x; e < kChunk / 4; e += kBwdThreads) {
+    const int t0 = cb + 4 * e;
+    const bool ok = t0 < L;
+    cp_async16(&rw.pos[4 * e], a.pos + (int64_t)r * L + (ok ? t0 : 0), ok ? 16 : 0);
+  }
+  if (cb > s0) {
+    for (int e = threadIdx.x; e < N * (kBwdCh / 4); e += kBwdThreads) {
+      const int n = e / (kBwdCh / 4), q = e % (kBwdCh / 4);
+      const int d0 = dblk * kBwdCh + 4 * q;
+      const bool ok = d0 < Dn;
+      const float* src = a.states + (((int64_t)r * a.nchunk + c) * N + n) * Dn + (ok ? d0 : 0);
+      cp_async16(&rw.st[n][4 * q], src, ok ? 16 : 0);
+    }
+  }
+  cp_async_commit();
+}
+
 template <typename T, int N, bool kVec>
 __global__ void __launch_bounds__(kBwdThreads, 3)
 scan_bwd_kernel(const ScanBwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  using SM = BwdSmem<N>;
+  using SM = BwdSmem<T, N>;
   constexpr int NH = SM::NH, kQ = SM::kQ, kRows = SM::kRows;
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
@@ -305,36 +365,33 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
   const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
   float dD = 0.f, ddtb = 0.f;
-  int xbuf = 0;
 
   const int cfirst = s0 / kChunk, clast = (s1 - 1) / kChunk;
-  Raw8<T, kVec> pu, pt, py;  // prefetched raw rows: steps [cb + 8hf, +8)
-  {
-    const int64_t i0 = (int64_t)clast * kChunk + 8 * hf;
-    pu.load(u_row, i0, L);
-    pt.load(dt_row, i0, L);
-    py.load(dy_row, i0, L);
-  }
+  if constexpr (kVec) bwd_issue_raw<T, N>(sm.raw, a, r, dblk, clast, s0);
 
   for (int c = clast; c >= cfirst; --c) {
     const int cb = c * kChunk, c0 = max(cb, s0), c1 = min(cb + kChunk, s1);
-    // chunk start state (irrelevant when cb <= s0: s0 is a head)
+    if constexpr (kVec) cp_async_wait_all();
+    __syncthreads();  // raw chunk visible; previous chunk's smem readers done
+    // ---- phase 1: scalars, B/C, head, chunk start state ----
     float h[NH];
-    if (cb > s0) {
-      const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
-#pragma unroll
-      for (int j = 0; j < NH; ++j) h[j] = st[(int64_t)j * Dn];
-    } else {
-#pragma unroll
-      for (int j = 0; j < NH; ++j) h[j] = 0.f;
-    }
-    __syncthreads();  // previous chunk's readers of sd/su/sy/ss/B/C are done
-    // ---- phase 1: per-(t,d) scalars for steps [cb + 8hf, +8) ----
     {
       float uu[8], vv[8], yy[8];
-      pu.unpack(uu);
-      pt.unpack(vv);
-      py.unpack(yy);
+      if constexpr (kVec) {
+        const T* ru = &sm.raw.u[cl][8 * hf];
+        const T* rt = &sm.raw.dt[cl][8 * hf];
+        const T* ry = &sm.raw.dy[cl][8 * hf];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uu[i] = IO<T>::cvt(ru[i]);
+          vv[i] = IO<T>::cvt(rt[i]);
+          yy[i] = IO<T>::cvt(ry[i]);
+        }
+      } else {
+        load8<T, false>(u_row, cb + 8 * hf, L, uu);
+        load8<T, false>(dt_row, cb + 8 * hf, L, vv);
+        load8<T, false>(dy_row, cb + 8 * hf, L, yy);
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int ii = 8 * hf + i;
@@ -350,14 +407,38 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         sm.sy[ii][cl] = active ? yy[i] : 0.f;
         sm.ss[ii][cl] = sg;
       }
+      if constexpr (kVec) {
+        for (int e = tid; e < N * kChunk; e += kBwdThreads) {
+          const int n = e % N, t = e / N;
+          sm.B[t][n] = IO<T>::cvt(sm.raw.B[n][t]);
+          sm.C[t][n] = IO<T>::cvt(sm.raw.C[n][t]);
+        }
+        for (int e = tid; e < kChunk; e += kBwdThreads) {
+          const int t = cb + e;
+          sm.head[e] = (t >= L) ? 1 : (t == 0 || sm.raw.pos[e] == 0);
+        }
+        if (cb > s0) {
+#pragma unroll
+          for (int j = 0; j < NH; ++j) h[j] = sm.raw.st[n0 + j][cl];
+        } else {
+#pragma unroll
+          for (int j = 0; j < NH; ++j) h[j] = 0.f;
+        }
+      } else {
+        stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.head);
+        if (cb > s0) {
+          const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
+#pragma unroll
+          for (int j = 0; j < NH; ++j) h[j] = st[(int64_t)j * Dn];
+        } else {
+#pragma unroll
+          for (int j = 0; j < NH; ++j) h[j] = 0.f;
+        }
+      }
     }
-    stage_bc<T, N, kChunk, kVec>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.head);
-    __syncthreads();
-    if (c > cfirst) {  // prefetch the next (earlier) chunk while this one computes
-      const int64_t i0 = (int64_t)(c - 1) * kChunk + 8 * hf;
-      pu.load(u_row, i0, L);
-      pt.load(dt_row, i0, L);
-      py.load(dy_row, i0, L);
+    __syncthreads();  // scalars visible; raw buffer free
+    if constexpr (kVec) {
+      if (c > cfirst) bwd_issue_raw<T, N>(sm.raw, a, r, dblk, c - 1, s0);
     }
 
     // ---- pass A: forward over the chunk, record sub-chunk start states ----
@@ -482,33 +563,32 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
           acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
           acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 2);
-          if (row < kRows && ch == 0) sm.xw[xbuf][wid][row][rh] = acc;
+          if (row < kRows && ch == 0) sm.xw[sc * (kSub / 2) + round][wid][row][rh] = acc;
         }
-        __syncthreads();
-        // cross-warp sum: 2 steps x 2N values
-        for (int e = tid; e < 2 * 2 * N; e += kBwdThreads) {
-          const int s = e / (2 * N), v = e % (2 * N);
-          const int t = a0 + 2 * round + s;
-          if (t >= c0 && t < c1) {
-            const int n = v < N ? v : v - N;
-            const int rh = n / NH;
-            const int kk = (v < N ? 0 : NH) + n % NH;
-            const int row = s * kQ + kk / 4, comp = kk % 4;
-            float acc = 0.f;
-#pragma unroll
-            for (int w = 0; w < kBwdWarps; ++w) {
-              const float4 p = sm.xw[xbuf][w][row][rh];
-              acc += comp == 0 ? p.x : comp == 1 ? p.y : comp == 2 ? p.z : p.w;
-            }
-            ws_bc_r[(int64_t)t * (2 * N) + v] = acc;
-          }
-        }
-        xbuf ^= 1;
         __syncwarp();
       }
       if (active && hf == 0) {
         store4<T, kVec>(du_row, a0, c0, c1, duo);
         store4<T, kVec>(ddt_row, a0, c0, c1, ddo);
+      }
+    }
+    // ---- cross-warp sum of the chunk's dB/dC partials: one barrier ----
+    __syncthreads();
+    for (int e = tid; e < kChunk * 2 * N; e += kBwdThreads) {
+      const int s16 = e / (2 * N), v = e % (2 * N);
+      const int t = cb + s16;
+      if (t >= c0 && t < c1) {
+        const int n = v < N ? v : v - N;
+        const int rh = n / NH;
+        const int kk = (v < N ? 0 : NH) + n % NH;
+        const int row = (s16 & 1) * kQ + kk / 4, comp = kk % 4;
+        float acc = 0.f;
+#pragma unroll
+        for (int w = 0; w < kBwdWarps; ++w) {
+          const float4 p = sm.xw[s16 >> 1][w][row][rh];
+          acc += comp == 0 ? p.x : comp == 1 ? p.y : comp == 2 ? p.z : p.w;
+        }
+        ws_bc_r[(int64_t)t * (2 * N) + v] = acc;
       }
     }
   }
@@ -630,7 +710,7 @@ pm_status dispatch_fwd(const ScanFwdArgs& a, int N, bool vec, cudaStream_t s) {
 template <typename T, int N, bool kVec>
 pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, float* dD,
                      float* ddtb, cudaStream_t s) {
-  const size_t smem = sizeof(BwdSmem<N>);
+  const size_t smem = sizeof(BwdSmem<T, N>);
   auto kern = scan_bwd_kernel<T, N, kVec>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return PM_ERR_CUDA;
@@ -734,8 +814,9 @@ pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, c
                         (const void*)dD, (const void*)ddt_bias})
     if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
   const int isz = io == PM_F32 ? 4 : 2;
-  const bool vec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
-                   aligned16(C) && aligned16(dy) && aligned16(du) && aligned16(ddt);
+  const bool vec = (L * isz) % 16 == 0 && Dn % 4 == 0 && aligned16(u) && aligned16(dt) &&
+                   aligned16(B) && aligned16(C) && aligned16(dy) && aligned16(du) &&
+                   aligned16(ddt) && aligned16(states);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   char* w = static_cast<char*>(workspace);
