@@ -245,7 +245,7 @@ def max_over_ranks(torch, dist, world, v, dev):
 # ---------------------------------------------------------------------------
 
 def oracle_step(orc, cfg, sample):
-    """One oracle pass of the full path on a bounded sample (host fp64)."""
+    """One oracle pass of the full path on a sample (host fp64)."""
     x, dt, B, C, dy, pos, P, Dc = sample
     u = orc.conv_fwd(x, P["w"][:Dc], P["bias"][:Dc], pos)
     orc.scan_fwd(u, dt, P["A"][:Dc], B, C, P["D"][:Dc], P["dt_bias"][:Dc], pos)
@@ -253,40 +253,48 @@ def oracle_step(orc, cfg, sample):
     orc.conv_bwd(x, P["w"][:Dc], P["bias"][:Dc], pos, g["du"])
 
 
-def oracle_sample(torch, cfg, Dc, rows_layout):
-    """Row 0 of the workload, first Dc channels, as exact fp64 host arrays.
-    Inputs come from the seeded generator (never from the CUDA path)."""
-    pos, valid = workload.pos_from_rows(rows_layout[:1], cfg.L)
-    sub = workload.Shape(cfg.name, 1, cfg.L, cfg.Dn, cfg.N, cfg.K, cfg.dtype)
-    T = workload.row_tensors(torch, sub, [0], valid, device="cpu")
+def oracle_sample(torch, cfg, n_rows, Dc, rows_layout):
+    """The first n_rows rows of the workload, first Dc channels, as exact fp64
+    host arrays.  Inputs come from the seeded generator (never from the CUDA
+    path); the layout comes from the oracle's own planner."""
+    pos, valid = workload.pos_from_rows(rows_layout[:n_rows], cfg.L)
+    T = workload.row_tensors(torch, cfg, list(range(n_rows)), valid, device="cpu")
     P = {k: v.double().numpy() for k, v in workload.params(torch, cfg, device="cpu").items()}
     f = lambda t: t.double().numpy()
     return (f(T["x"])[:, :Dc].copy(), f(T["dt"])[:, :Dc].copy(), f(T["B"]), f(T["C"]),
             f(T["dy"])[:, :Dc].copy(), pos, P, Dc)
 
 
-def cpu_time_per_channel(torch, orc, cfg, rows_layout, Dc=16):
-    s = oracle_sample(torch, cfg, Dc, rows_layout)
+def size_sample(torch, orc, cfg, rows_layout, budget_s):
+    """Pick (rows, channels) so one oracle step takes about budget_s."""
+    s = oracle_sample(torch, cfg, 1, 64, rows_layout)
     t0 = time.perf_counter()
     oracle_step(orc, cfg, s)
-    return (time.perf_counter() - t0) / Dc
+    per_ch = (time.perf_counter() - t0) / 64  # seconds per (row, channel)
+    units = max(1, int(budget_s / max(per_ch, 1e-9)))
+    if units >= cfg.Dn:
+        return min(cfg.R, units // cfg.Dn), cfg.Dn
+    return 1, max(16, units)
 
 
-def cpu_baseline(torch, cfg, target_s=12.0):
+def describe(n_rows, Dc, cfg, secs):
+    return (f"{n_rows} row(s) x {Dc} of {cfg.Dn} channels x L={cfg.L} of the {cfg.name} workload "
+            f"(fp64 oracle: conv fwd, scan fwd, scan bwd, conv bwd), {secs:.1f} s per pass; "
+            f"slots scaled by {Dc}/{cfg.Dn}")
+
+
+def cpu_baseline(torch, cfg, target_s=15.0):
     import oracle as orc
     lens, row, off = build_layout_host(cfg)  # oracle planner: no input from the CUDA path
     rows_layout = workload.rows_from_plan(lens, row, off, cfg.R)
-    per_ch = cpu_time_per_channel(torch, orc, cfg, rows_layout)
-    Dc = int(max(16, min(cfg.Dn, target_s / max(per_ch, 1e-9))))
-    s = oracle_sample(torch, cfg, Dc, rows_layout)
+    n_rows, Dc = size_sample(torch, orc, cfg, rows_layout, target_s)
+    s = oracle_sample(torch, cfg, n_rows, Dc, rows_layout)
     t0 = time.perf_counter()
     oracle_step(orc, cfg, s)
     dt = time.perf_counter() - t0
-    slots = cfg.L * Dc / cfg.Dn  # channel-fraction-scaled slots of the sample
+    slots = n_rows * cfg.L * Dc / cfg.Dn  # channel-fraction-scaled slots of the sample
     return {"value": slots / dt, "unit": UNIT, "cores": orc.num_threads(), "kind": "oracle",
-            "sample": f"1 row x {Dc} of {cfg.Dn} channels x L={cfg.L} (conv fwd, scan fwd, "
-                      f"scan bwd, conv bwd in fp64), {dt:.1f} s, slots scaled by "
-                      f"{Dc}/{cfg.Dn}"}
+            "sample": describe(n_rows, Dc, cfg, dt)}
 
 
 def run_reference(args, cfg):
@@ -298,20 +306,18 @@ def run_reference(args, cfg):
     import oracle as orc
     lens, row, off = build_layout_host(cfg)
     rows_layout = workload.rows_from_plan(lens, row, off, cfg.R)
-    per_ch = cpu_time_per_channel(torch, orc, cfg, rows_layout)
     budget = 150.0 / max(1, args.steps + args.warmup)
-    Dc = int(max(16, min(cfg.Dn, budget / max(per_ch, 1e-9))))
-    s = oracle_sample(torch, cfg, Dc, rows_layout)
+    n_rows, Dc = size_sample(torch, orc, cfg, rows_layout, budget)
+    s = oracle_sample(torch, cfg, n_rows, Dc, rows_layout)
     for _ in range(args.warmup):
         oracle_step(orc, cfg, s)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         oracle_step(orc, cfg, s)
     el = (time.perf_counter() - t0) / args.steps
-    slots = cfg.L * Dc / cfg.Dn
+    slots = n_rows * cfg.L * Dc / cfg.Dn
     v = slots / el
-    sample = (f"1 row x {Dc} of {cfg.Dn} channels x L={cfg.L} per step (fp64 oracle: conv fwd, "
-              f"scan fwd, scan bwd, conv bwd), slots scaled by {Dc}/{cfg.Dn}")
+    sample = describe(n_rows, Dc, cfg, el)
     out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": el * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -1,0 +1,91 @@
+"""Full-size parity at BASELINE.json shapes, in the launch configuration
+bench.py times (all rows of a GPU in one launch of each kernel).
+
+The fp64 oracle cannot run every row in seconds, so each test samples rows:
+the per-token outputs of a sampled row from the FULL launch are compared
+element by element with the oracle fed that row's exact GPU inputs; the
+parameter gradients (sums over all rows) are checked (a) on a single-row
+launch against the oracle and (b) on the full launch through properties
+that hold at any size (dD = sum dy*u; dbias = sum dpre recomputed in fp64)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import paper_2408_03865_b200 as pm
+import workload
+from tests._common import TOL, rel_err, to_np
+
+pytestmark = pytest.mark.gpu
+
+
+def build(cfg, R=None, seed_rows=None):
+    R = R or cfg.R
+    n = int(R * cfg.L / 500) + 64
+    while True:
+        lens = workload.lengths_stream(cfg.name, n)
+        row, off, nr = oracle.plan_fifo(lens, cfg.L)
+        if nr - 1 >= R:
+            break
+        n *= 2
+    keep = row < R
+    rows = workload.rows_from_plan(lens[keep], row[keep], off[keep], R)
+    pos_np, valid = workload.pos_from_rows(rows, cfg.L)
+    shape = workload.Shape(cfg.name, R, cfg.L, cfg.Dn, cfg.N, cfg.K, cfg.dtype)
+    T = workload.row_tensors(torch, shape, list(range(R)), valid, device="cuda")
+    P = workload.params(torch, shape, device="cuda")
+    return pos_np, valid, T, P
+
+
+def chain(pos, T, P):
+    u = pm.pm_causal_conv1d_fwd(T["x"], P["w"], P["bias"], pos)
+    y, st = pm.pm_selective_scan_fwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos)
+    g = pm.pm_selective_scan_bwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos,
+                                 T["dy"], states=st)
+    dx, dw, db = pm.pm_causal_conv1d_bwd(T["x"], P["w"], P["bias"], pos, g["du"])
+    torch.cuda.synchronize()
+    return dict(u=u, y=y, dx=dx, dw=dw, db=db, **g)
+
+
+def row_np(t, r):
+    return to_np(t[r:r + 1])
+
+
+@pytest.mark.parametrize("name,R", [("1.4b", 8), ("2.8b-16k", 8)])
+def test_fullsize_sampled_rows(name, R):
+    cfg = workload.CONFIGS[name]
+    io = cfg.dtype
+    pos_np, valid, T, P = build(cfg, R)
+    pos = torch.as_tensor(pos_np, device="cuda")
+    out = chain(pos, T, P)
+    p = {k: to_np(v) for k, v in P.items()}
+    r = R - 1  # sampled row (last row: ends in padding)
+    pr = pos_np[r:r + 1]
+    x = row_np(T["x"], r)
+    ru = oracle.conv_fwd(x, p["w"], p["bias"], pr)
+    assert rel_err(row_np(out["u"], r), ru) <= TOL[(io, "fwd")]
+    u = row_np(out["u"], r)
+    args = (u, row_np(T["dt"], r), p["A"], row_np(T["B"], r), row_np(T["C"], r), p["D"],
+            p["dt_bias"], pr)
+    assert rel_err(row_np(out["y"], r), oracle.scan_fwd(*args)) <= TOL[(io, "fwd")]
+    g = oracle.scan_bwd(*args, row_np(T["dy"], r))
+    for k in ("du", "ddt", "dB", "dC"):
+        e = rel_err(row_np(out[k], r), g[k])
+        assert e <= TOL[(io, "bwd")], (k, e)
+    rdx, _, _ = oracle.conv_bwd(x, p["w"], p["bias"], pr, row_np(out["du"], r))
+    assert rel_err(row_np(out["dx"], r), rdx) <= TOL[(io, "bwd")]
+    # (b) properties of the full launch: dD[d] = sum_{r,t} dy * u
+    dD = (T["dy"].double() * out["u"].double()).sum(dim=(0, 2)).cpu().numpy()
+    assert rel_err(to_np(out["dD"]), dD) <= TOL[(io, "bwd")]
+    # (a) single-row launch: parameter gradients vs the oracle
+    T1 = {k: v[r:r + 1].contiguous() for k, v in T.items()}
+    o1 = chain(pos[r:r + 1].contiguous(), T1, P)
+    for k in ("du", "ddt", "dB", "dC", "y", "u"):  # same row, different launch shape
+        assert torch.equal(o1[k][0], out[k][r]), k
+    for k, ref in (("dA", g["dA"]), ("dD", g["dD"]), ("ddt_bias", g["ddt_bias"])):
+        e = rel_err(to_np(o1[k]), ref)
+        assert e <= TOL[(io, "bwd")], (k, e)
+    _, rdw, rdb = oracle.conv_bwd(x, p["w"], p["bias"], pr, to_np(o1["du"]))
+    assert rel_err(to_np(o1["dw"]), rdw) <= TOL[(io, "bwd")]
+    assert rel_err(to_np(o1["db"]), rdb) <= TOL[(io, "bwd")]
