@@ -201,9 +201,10 @@ scan_fwd_kernel(const ScanFwdArgs a) {
 #pragma unroll
         for (int n = 0; n < N; ++n) h[n] = fmaf(ex2(delta * A2[n]), h[n], dux * Bt[n]);
       }
+      float yp[4] = {yv, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int n = 0; n < N; ++n) yv = fmaf(Ct[n], h[n], yv);
-      yy[i] = yv;
+      for (int n = 0; n < N; ++n) yp[n & 3] = fmaf(Ct[n], h[n], yp[n & 3]);
+      yy[i] = (yp[0] + yp[1]) + (yp[2] + yp[3]);
     }
     if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
   }
@@ -521,20 +522,21 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           const bool head = sm.head[ii];
           const float* Bt = &sm.B[ii][n0];
           const float* Ct = &sm.C[ii][n0];
-          float Ssum = 0.f, dq = 0.f;
+          float Sp[2] = {0.f, 0.f}, dqp[2] = {0.f, 0.f};  // split chains
           float vals[N];  // [dB of my NH states | dC of my NH states]
 #pragma unroll
           for (int j = 0; j < NH; ++j) {
             g[j] = fmaf(Ct[j], dyv, g[j]);  // g holds abar_{t+1} g_{t+1}
-            Ssum = fmaf(g[j], Bt[j], Ssum);
+            Sp[j & 1] = fmaf(g[j], Bt[j], Sp[j & 1]);
             const float hm = head ? 0.f : fmaf(-dux, Bt[j], hb[i][j]);  // abar_t h_{t-1}
             const float q = g[j] * hm;
             dA[j] = fmaf(delta, q, dA[j]);
-            dq = fmaf(A2[j], q, dq);
+            dqp[j & 1] = fmaf(A2[j], q, dqp[j & 1]);
             vals[j] = g[j] * dux;
             vals[NH + j] = dyv * hb[i][j];
             g[j] = ab[i][j] * g[j];  // carry to t-1 (0 at heads)
           }
+          float Ssum = Sp[0] + Sp[1], dq = dqp[0] + dqp[1];
 #pragma unroll
           for (int q = 0; q < kQ; ++q)
             rrow[q * kRedStride] = make_float4(vals[4 * q], vals[4 * q + 1], vals[4 * q + 2], vals[4 * q + 3]);
@@ -574,21 +576,23 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     }
     // ---- cross-warp sum of the chunk's dB/dC partials: one barrier ----
     __syncthreads();
-    for (int e = tid; e < kChunk * 2 * N; e += kBwdThreads) {
-      const int s16 = e / (2 * N), v = e % (2 * N);
-      const int t = cb + s16;
-      if (t >= c0 && t < c1) {
-        const int n = v < N ? v : v - N;
-        const int rh = n / NH;
-        const int kk = (v < N ? 0 : NH) + n % NH;
-        const int row = (s16 & 1) * kQ + kk / 4, comp = kk % 4;
-        float acc = 0.f;
+    {
+      const float* xwf = reinterpret_cast<const float*>(&sm.xw[0][0][0][0]);
+      constexpr int kWStride = kRows * 2 * 4;  // floats between warps
+      for (int e = tid; e < kChunk * 2 * N; e += kBwdThreads) {
+        const int s16 = e / (2 * N), v = e % (2 * N);
+        const int t = cb + s16;
+        if (t >= c0 && t < c1) {
+          const int n = v < N ? v : v - N;
+          const int rh = n / NH;
+          const int kk = (v < N ? 0 : NH) + n % NH;
+          const int row = (s16 & 1) * kQ + kk / 4;
+          const float* p = xwf + ((((s16 >> 1) * kBwdWarps) * kRows + row) * 2 + rh) * 4 + (kk & 3);
+          float acc = 0.f;
 #pragma unroll
-        for (int w = 0; w < kBwdWarps; ++w) {
-          const float4 p = sm.xw[s16 >> 1][w][row][rh];
-          acc += comp == 0 ? p.x : comp == 1 ? p.y : comp == 2 ? p.z : p.w;
+          for (int w = 0; w < kBwdWarps; ++w) acc += p[w * kWStride];
+          ws_bc_r[(int64_t)t * (2 * N) + v] = acc;
         }
-        ws_bc_r[(int64_t)t * (2 * N) + v] = acc;
       }
     }
   }
