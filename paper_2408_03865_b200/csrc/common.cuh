@@ -28,9 +28,30 @@ PM_DEV float rcp(float x) {  // MUFU.RCP
 }
 PM_DEV float sigmoidf_fast(float v) { return rcp(1.f + ex2(-v * kLog2e)); }
 
-// softplus(v) = log(1 + e^v); linear tail above 20 (error < 2e-9 relative,
-// reading Q4).  log1pf keeps full fp32 accuracy for small e^v (delta ~1e-4).
-PM_DEV float softplusf(float v) { return v > 20.f ? v : log1pf(ex2(v * kLog2e)); }
+PM_DEV float lg2(float x) {  // MUFU.LG2
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// softplus(v) = log(1 + x), x = e^v (reading Q4).  Branch-free and short:
+//  * x < 1/32: 5-term Taylor series of log1p (relative error < x^5/6 < 2e-9)
+//    -- keeps full accuracy where delta is tiny (dt ~ 1e-4);
+//  * x >= 1/32: lg2.approx(1 + x) * ln2 (absolute error ~1.7e-7, i.e.
+//    < 6e-6 relative since log1p(x) >= 0.03 there);
+//  * v > 20: v (error < 2e-9 relative).
+// Also returns x (callers derive sigmoid(v) = x / (1 + x) from it).
+PM_DEV float softplus_x(float v, float& x) {
+  x = ex2(v * kLog2e);
+  const float p = x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, 0.2f, -0.25f), 0.33333334f), -0.5f), 1.f);
+  const float l = lg2(1.f + x) * kLn2;
+  const float d = x < 0.03125f ? p : l;
+  return v > 20.f ? v : d;
+}
+PM_DEV float softplusf(float v) {
+  float x;
+  return softplus_x(v, x);
+}
 
 // ----------------------------------------------------------------- I/O ----
 template <typename T> struct IO;

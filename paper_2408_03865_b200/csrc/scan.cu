@@ -20,6 +20,7 @@
 //    shared memory, then over warps, into per-channel-block partials that a
 //    finalize kernel sums in a fixed order (deterministic).
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -120,7 +121,7 @@ struct Raw8<__nv_bfloat16, true> {
 // forward
 // ---------------------------------------------------------------------------
 template <typename T, int N, bool kVec>
-__global__ void __launch_bounds__(kScanThreads)
+__global__ void __launch_bounds__(kScanThreads, 4)
 scan_fwd_kernel(const ScanFwdArgs a) {
   __shared__ __align__(16) float sB[kTile][N];
   __shared__ __align__(16) float sC[kTile][N];
@@ -157,7 +158,8 @@ scan_fwd_kernel(const ScanFwdArgs a) {
 
   // Flat loop over 8-step sub-blocks; u/dt of the next sub-block are loaded
   // into registers before the current one is computed (software pipeline),
-  // B/C/head tiles are restaged at every kTile boundary.
+  // B/C/head tiles are restaged at every kTile boundary.  Sub-blocks fully
+  // inside the segment (all but at most two) run without per-step checks.
   int tb = s0 & ~7;
   Raw8<T, kVec> pu, pt;
   pu.load(u_row, tb, L);
@@ -178,34 +180,39 @@ scan_fwd_kernel(const ScanFwdArgs a) {
       pt.load(dt_row, tb + 8, L);
     }
     const int sb = tb - j0;
+    // checkpoint = state before step tb (only step i == 0 can be a multiple of kChunk)
+    if (a.states != nullptr && (tb % kChunk) == 0 && tb >= s0 && active) {
+      float* st = a.states + (((int64_t)r * a.nchunk + tb / kChunk) * N) * Dn + d;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int t = tb + i;
-      yy[i] = 0.f;
-      if (t < s0 || t >= s1) continue;  // CTA-uniform
-      if (a.states != nullptr && (t % kChunk) == 0 && active) {
-        float* st = a.states + (((int64_t)r * a.nchunk + t / kChunk) * N) * Dn + d;
-#pragma unroll
-        for (int n = 0; n < N; ++n) st[(int64_t)n * Dn] = h[n];
-      }
-      const float v = vv[i] + bias;
-      const float delta = a.softplus ? softplusf(v) : v;
-      const float dux = delta * uu[i];
-      float yv = Dd * uu[i];
-      const float* Bt = sB[sb + i];
-      const float* Ct = sC[sb + i];
-      if (sHead[sb + i]) {
-#pragma unroll
-        for (int n = 0; n < N; ++n) h[n] = dux * Bt[n];
-      } else {
-#pragma unroll
-        for (int n = 0; n < N; ++n) h[n] = fmaf(ex2(delta * A2[n]), h[n], dux * Bt[n]);
-      }
-      float yp[4] = {yv, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int n = 0; n < N; ++n) yp[n & 3] = fmaf(Ct[n], h[n], yp[n & 3]);
-      yy[i] = (yp[0] + yp[1]) + (yp[2] + yp[3]);
+      for (int n = 0; n < N; ++n) st[(int64_t)n * Dn] = h[n];
     }
+    auto block = [&](auto full_tag) {
+      constexpr bool kFull = decltype(full_tag)::value;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int t = tb + i;
+        yy[i] = 0.f;
+        if (!kFull && (t < s0 || t >= s1)) continue;  // CTA-uniform
+        const float v = vv[i] + bias;
+        const float delta = a.softplus ? softplusf(v) : v;
+        const float dux = delta * uu[i];
+        const float* Bt = sB[sb + i];
+        const float* Ct = sC[sb + i];
+        if (sHead[sb + i]) {
+#pragma unroll
+          for (int n = 0; n < N; ++n) h[n] = dux * Bt[n];
+        } else {
+#pragma unroll
+          for (int n = 0; n < N; ++n) h[n] = fmaf(ex2(delta * A2[n]), h[n], dux * Bt[n]);
+        }
+        float yp[4] = {Dd * uu[i], 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int n = 0; n < N; ++n) yp[n & 3] = fmaf(Ct[n], h[n], yp[n & 3]);
+        yy[i] = (yp[0] + yp[1]) + (yp[2] + yp[3]);
+      }
+    };
+    if (tb >= s0 && tb + 8 <= s1) block(std::true_type{});
+    else block(std::false_type{});
     if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
   }
 }
@@ -255,10 +262,8 @@ struct BwdSmem {
   static constexpr int kQ = N / 4;   // float4 quads of (dB, dC) values per thread-step
   static constexpr int kRows = 2 * kQ;  // transpose rows per 2-step round
   BwdRaw<T, N> raw;
-  float sd[kChunk][kBwdCh];   // delta
-  float su[kChunk][kBwdCh];   // u (0 on inactive channels)
-  float sy[kChunk][kBwdCh];   // dy (0 on inactive channels)
-  float ss[kChunk][kBwdCh];   // softplus'(v) (1 if softplus off)
+  float4 sc[kChunk][kBwdCh];  // per-(t,d) scalars {delta, u, dy, softplus'(v)}
+                              // (u = dy = 0 on inactive channels)
   float2 sub[kNSub][NH / 2][kBwdThreads];  // sub-chunk start states
   float4 red[kBwdWarps][kRows][kRedStride];
   float4 xw[kChunk / 2][kBwdWarps][kRows][2];
@@ -399,14 +404,11 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         const float v = vv[i] + bias;
         float dl = v, sg = 1.f;
         if (a.softplus) {
-          const float e = ex2(v * kLog2e);
-          dl = v > 20.f ? v : log1pf(e);
-          sg = v > 20.f ? 1.f : __fdividef(e, 1.f + e);
+          float x;
+          dl = softplus_x(v, x);
+          sg = v > 20.f ? 1.f : __fdividef(x, 1.f + x);
         }
-        sm.sd[ii][cl] = dl;
-        sm.su[ii][cl] = active ? uu[i] : 0.f;
-        sm.sy[ii][cl] = active ? yy[i] : 0.f;
-        sm.ss[ii][cl] = sg;
+        sm.sc[ii][cl] = make_float4(dl, active ? uu[i] : 0.f, active ? yy[i] : 0.f, sg);
       }
       if constexpr (kVec) {
         for (int e = tid; e < N * kChunk; e += kBwdThreads) {
@@ -442,6 +444,8 @@ scan_bwd_kernel(const ScanBwdArgs a) {
       if (c > cfirst) bwd_issue_raw<T, N>(sm.raw, a, r, dblk, c - 1, s0);
     }
 
+    auto passes = [&](auto full_tag) {
+      constexpr bool kFull = decltype(full_tag)::value;
     // ---- pass A: forward over the chunk, record sub-chunk start states ----
 #pragma unroll
     for (int ii = 0; ii < kChunk; ++ii) {
@@ -451,9 +455,10 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         for (int q = 0; q < NH / 2; ++q)
           sm.sub[ii / kSub][q][tid] = make_float2(h[2 * q], h[2 * q + 1]);
       }
-      if (t < c0 || t >= c1) continue;  // CTA-uniform
-      const float delta = sm.sd[ii][cl];
-      const float dux = delta * sm.su[ii][cl];
+      if (!kFull && (t < c0 || t >= c1)) continue;  // CTA-uniform
+      const float4 scv = sm.sc[ii][cl];
+      const float delta = scv.x;
+      const float dux = delta * scv.y;
       const float* Bt = &sm.B[ii][n0];
       if (sm.head[ii]) {
 #pragma unroll
@@ -467,7 +472,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     // ---- pass B: sub-chunks in reverse ----
     for (int sc = kNSub - 1; sc >= 0; --sc) {
       const int a0 = cb + sc * kSub;
-      if (a0 >= c1 || a0 + kSub <= c0) continue;  // CTA-uniform
+      if (!kFull && (a0 >= c1 || a0 + kSub <= c0)) continue;  // CTA-uniform
       float hb[kSub][NH], ab[kSub][NH];
 #pragma unroll
       for (int q = 0; q < NH / 2; ++q) {
@@ -478,9 +483,10 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 #pragma unroll
       for (int i = 0; i < kSub; ++i) {
         const int t = a0 + i, ii = t - cb;
-        if (t >= c0 && t < c1) {  // CTA-uniform
-          const float delta = sm.sd[ii][cl];
-          const float dux = delta * sm.su[ii][cl];
+        if (kFull || (t >= c0 && t < c1)) {  // CTA-uniform
+          const float4 scv = sm.sc[ii][cl];
+          const float delta = scv.x;
+          const float dux = delta * scv.y;
           const float* Bt = &sm.B[ii][n0];
           if (sm.head[ii]) {
 #pragma unroll
@@ -510,14 +516,15 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           const int i = 2 * round + s;
           const int t = a0 + i, ii = t - cb;
           float4* rrow = &sm.red[wid][s * kQ][lid];
-          if (t < c0 || t >= c1) {  // CTA-uniform
+          if (!kFull && (t < c0 || t >= c1)) {  // CTA-uniform
 #pragma unroll
             for (int q = 0; q < kQ; ++q) rrow[q * kRedStride] = make_float4(0.f, 0.f, 0.f, 0.f);
             duo[i] = 0.f;
             ddo[i] = 0.f;
             continue;
           }
-          const float delta = sm.sd[ii][cl], ux = sm.su[ii][cl], dyv = sm.sy[ii][cl];
+          const float4 scv = sm.sc[ii][cl];
+          const float delta = scv.x, ux = scv.y, dyv = scv.z;
           const float dux = delta * ux;
           const bool head = sm.head[ii];
           const float* Bt = &sm.B[ii][n0];
@@ -543,7 +550,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           Ssum += __shfl_xor_sync(0xffffffffu, Ssum, 1);
           dq += __shfl_xor_sync(0xffffffffu, dq, 1);
           duo[i] = fmaf(Dd, dyv, delta * Ssum);
-          ddo[i] = fmaf(ux, Ssum, dq * kLn2) * sm.ss[ii][cl];
+          ddo[i] = fmaf(ux, Ssum, dq * kLn2) * scv.w;
           dD = fmaf(dyv, ux, dD);
           ddtb += ddo[i];
         }
@@ -570,10 +577,18 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         __syncwarp();
       }
       if (active && hf == 0) {
-        store4<T, kVec>(du_row, a0, c0, c1, duo);
-        store4<T, kVec>(ddt_row, a0, c0, c1, ddo);
+        if (kFull) {
+          store4<T, kVec>(du_row, a0, a0, a0 + kSub, duo);
+          store4<T, kVec>(ddt_row, a0, a0, a0 + kSub, ddo);
+        } else {
+          store4<T, kVec>(du_row, a0, c0, c1, duo);
+          store4<T, kVec>(ddt_row, a0, c0, c1, ddo);
+        }
       }
     }
+    };
+    if (c0 == cb && c1 == cb + kChunk) passes(std::true_type{});
+    else passes(std::false_type{});
     // ---- cross-warp sum of the chunk's dB/dC partials: one barrier ----
     __syncthreads();
     {
@@ -670,7 +685,7 @@ int n_segments(int64_t R, int64_t nblk, int64_t L, int64_t resident_per_sm) {
   s = std::max<int64_t>(s, 1);
   return (int)std::min<int64_t>(s, 64);
 }
-int nseg_fwd(int64_t R, int64_t Dn, int64_t L) { return n_segments(R, n_dblk(Dn), L, 6); }
+int nseg_fwd(int64_t R, int64_t Dn, int64_t L) { return n_segments(R, n_dblk(Dn), L, 4); }
 int nseg_bwd(int64_t R, int64_t Dn, int64_t L) { return n_segments(R, n_dblk_bwd(Dn), L, 3); }
 
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
