@@ -156,6 +156,21 @@ PM_DEV void store4(T* __restrict__ p, int64_t i, int64_t lo, int64_t hi, const f
   }
 }
 
+template <typename T, bool kVec>
+PM_DEV void store2(T* __restrict__ p, int64_t i, int64_t lo, int64_t hi, const float (&v)[2]) {
+  if (kVec && i >= lo && i + 2 <= hi) {
+    if constexpr (sizeof(T) == 2) {
+      *reinterpret_cast<__nv_bfloat162*>(p + i) = __floats2bfloat162_rn(v[0], v[1]);
+    } else {
+      *reinterpret_cast<float2*>(p + i) = make_float2(v[0], v[1]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      if (i + k >= lo && i + k < hi) IO<T>::st(p + i + k, v[k]);
+  }
+}
+
 // ------------------------------------------------------------ cp.async ----
 // 16-byte global->shared async copy (LDGSTS); src_bytes < 16 zero-fills.
 PM_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -165,6 +180,74 @@ PM_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
 }
 PM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 PM_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// ---------------------------------------------------------------- TMEM ----
+// Tensor memory used as per-thread scratch: a warp's 32 threads own the 32
+// TMEM lanes of quarter (warp % 4); a thread's values sit in consecutive
+// 32-bit columns of its lane.  (sm_100a tcgen05; allocation in powers of 2
+// >= 32 columns by one warp, which also deallocates.)
+PM_DEV void tmem_alloc(uint32_t* smem_dst, uint32_t ncols) {  // whole warp
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(s), "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+PM_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {  // whole warp (the allocating one)
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols)
+               : "memory");
+}
+PM_DEV void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+PM_DEV void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+PM_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+PM_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+template <int M>  // store M (2, 4 or 8) fp32 values to columns [c, c+M) of my lane
+PM_DEV void tmem_st(uint32_t taddr, const float* v) {
+  if constexpr (M == 8) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+        : "memory");
+  } else if constexpr (M == 4) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+                 "r"(__float_as_uint(v[3]))
+                 : "memory");
+  } else {
+    static_assert(M == 2, "M in {2, 4, 8}");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr),
+                 "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1]))
+                 : "memory");
+  }
+}
+
+template <int M>  // load M values from columns [c, c+M) of my lane (call tmem_wait_ld before use)
+PM_DEV void tmem_ld(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  if constexpr (M == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "r"(taddr)
+                 : "memory");
+  } else if constexpr (M == 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr)
+                 : "memory");
+  } else {
+    static_assert(M == 2, "M in {2, 4, 8}");
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n"
+                 : "=r"(r[0]), "=r"(r[1])
+                 : "r"(taddr)
+                 : "memory");
+  }
+  tmem_wait_ld();
+#pragma unroll
+  for (int k = 0; k < M; ++k) v[k] = __uint_as_float(r[k]);
+}
 
 // --------------------------------------------------- segment splitting ----
 // A packed row is a concatenation of independent sequences (no

@@ -242,7 +242,9 @@ scan_fwd_kernel(const ScanFwdArgs a) {
 constexpr int kBwdCh = 64;                   // channels per CTA
 constexpr int kBwdThreads = 2 * kBwdCh;      // lane pair per channel
 constexpr int kBwdWarps = kBwdThreads / 32;
-constexpr int kRedStride = 36;               // float4 per transpose row (== 4 mod 8)
+constexpr int kRedStride = 32;               // float4 per transpose row (no padding)
+constexpr int kBSub = 2;                     // bwd register sub-chunk (= one reduction round)
+constexpr int kBNSub = kChunk / kBSub;
 static_assert(kChunk == 16, "phase 1 maps 8 steps to each thread of a pair");
 
 template <typename T, int N>
@@ -264,13 +266,13 @@ struct BwdSmem {
   BwdRaw<T, N> raw;
   float4 sc[kChunk][kBwdCh];  // per-(t,d) scalars {delta, u, dy, softplus'(v)}
                               // (u = dy = 0 on inactive channels)
-  float2 sub[kNSub][NH / 2][kBwdThreads];  // sub-chunk start states
   float4 red[kBwdWarps][kRows][kRedStride];
   float4 xw[kChunk / 2][kBwdWarps][kRows][2];
   float B[kChunk][N];
   float C[kChunk][N];
   int head[kChunk];
   int s_red[kBwdWarps];
+  uint32_t tmem_base;
 };
 
 // Issue the cp.async copies of chunk c's raw inputs (vector path only:
@@ -319,7 +321,7 @@ PM_DEV void bwd_issue_raw(BwdRaw<T, N>& rw, const ScanBwdArgs& a, int r, int dbl
 }
 
 template <typename T, int N, bool kVec>
-__global__ void __launch_bounds__(kBwdThreads, 3)
+__global__ void __launch_bounds__(kBwdThreads, 4)
 scan_bwd_kernel(const ScanBwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using SM = BwdSmem<T, N>;
@@ -350,6 +352,14 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     }
     return;
   }
+  // sub-chunk start states live in tensor memory (one TMEM lane per thread,
+  // kBNSub * NH fp32 columns), freeing shared memory for a 4th CTA per SM.
+  constexpr uint32_t kTmemCols = (kBNSub * NH <= 32) ? 32u : (kBNSub * NH <= 64 ? 64u : 128u);
+  if (wid == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = sm.tmem_base + ((uint32_t)((wid & 3) * 32) << 16);
 
   const T* B_r = static_cast<const T*>(a.B) + (int64_t)r * N * L;
   const T* C_r = static_cast<const T*>(a.C) + (int64_t)r * N * L;
@@ -450,11 +460,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 #pragma unroll
     for (int ii = 0; ii < kChunk; ++ii) {
       const int t = cb + ii;
-      if (ii % kSub == 0) {
-#pragma unroll
-        for (int q = 0; q < NH / 2; ++q)
-          sm.sub[ii / kSub][q][tid] = make_float2(h[2 * q], h[2 * q + 1]);
-      }
+      if (ii % kBSub == 0) tmem_st<NH>(tbase + (uint32_t)((ii / kBSub) * NH), h);
       if (!kFull && (t < c0 || t >= c1)) continue;  // CTA-uniform
       const float4 scv = sm.sc[ii][cl];
       const float delta = scv.x;
@@ -469,19 +475,15 @@ scan_bwd_kernel(const ScanBwdArgs a) {
       }
     }
 
-    // ---- pass B: sub-chunks in reverse ----
-    for (int sc = kNSub - 1; sc >= 0; --sc) {
-      const int a0 = cb + sc * kSub;
-      if (!kFull && (a0 >= c1 || a0 + kSub <= c0)) continue;  // CTA-uniform
-      float hb[kSub][NH], ab[kSub][NH];
+    tmem_wait_st();  // sub-chunk states are in TMEM before pass B reads them
+    // ---- pass B: 2-step sub-chunks in reverse (= one reduction round) ----
+    for (int sc = kBNSub - 1; sc >= 0; --sc) {
+      const int a0 = cb + sc * kBSub;
+      if (!kFull && (a0 >= c1 || a0 + kBSub <= c0)) continue;  // CTA-uniform
+      float hb[kBSub][NH], ab[kBSub][NH];
+      tmem_ld<NH>(tbase + (uint32_t)(sc * NH), h);
 #pragma unroll
-      for (int q = 0; q < NH / 2; ++q) {
-        const float2 s2 = sm.sub[sc][q][tid];
-        h[2 * q] = s2.x;
-        h[2 * q + 1] = s2.y;
-      }
-#pragma unroll
-      for (int i = 0; i < kSub; ++i) {
+      for (int i = 0; i < kBSub; ++i) {
         const int t = a0 + i, ii = t - cb;
         if (kFull || (t >= c0 && t < c1)) {  // CTA-uniform
           const float4 scv = sm.sc[ii][cl];
@@ -508,81 +510,81 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 #pragma unroll
         for (int j = 0; j < NH; ++j) hb[i][j] = h[j];
       }
-      float duo[kSub], ddo[kSub];
+      float duo[kBSub], ddo[kBSub];
 #pragma unroll
-      for (int round = kSub / 2 - 1; round >= 0; --round) {
+      for (int i = kBSub - 1; i >= 0; --i) {
+        const int t = a0 + i, ii = t - cb;
+        // row (i*kQ + q), column lid: row-wise writes are conflict-free
+        auto rslot = [&](int q) -> float4& { return sm.red[wid][i * kQ + q][lid]; };
+        if (!kFull && (t < c0 || t >= c1)) {  // CTA-uniform
 #pragma unroll
-        for (int s = 1; s >= 0; --s) {
-          const int i = 2 * round + s;
-          const int t = a0 + i, ii = t - cb;
-          float4* rrow = &sm.red[wid][s * kQ][lid];
-          if (!kFull && (t < c0 || t >= c1)) {  // CTA-uniform
-#pragma unroll
-            for (int q = 0; q < kQ; ++q) rrow[q * kRedStride] = make_float4(0.f, 0.f, 0.f, 0.f);
-            duo[i] = 0.f;
-            ddo[i] = 0.f;
-            continue;
-          }
-          const float4 scv = sm.sc[ii][cl];
-          const float delta = scv.x, ux = scv.y, dyv = scv.z;
-          const float dux = delta * ux;
-          const bool head = sm.head[ii];
-          const float* Bt = &sm.B[ii][n0];
-          const float* Ct = &sm.C[ii][n0];
-          float Sp[2] = {0.f, 0.f}, dqp[2] = {0.f, 0.f};  // split chains
-          float vals[N];  // [dB of my NH states | dC of my NH states]
-#pragma unroll
-          for (int j = 0; j < NH; ++j) {
-            g[j] = fmaf(Ct[j], dyv, g[j]);  // g holds abar_{t+1} g_{t+1}
-            Sp[j & 1] = fmaf(g[j], Bt[j], Sp[j & 1]);
-            const float hm = head ? 0.f : fmaf(-dux, Bt[j], hb[i][j]);  // abar_t h_{t-1}
-            const float q = g[j] * hm;
-            dA[j] = fmaf(delta, q, dA[j]);
-            dqp[j & 1] = fmaf(A2[j], q, dqp[j & 1]);
-            vals[j] = g[j] * dux;
-            vals[NH + j] = dyv * hb[i][j];
-            g[j] = ab[i][j] * g[j];  // carry to t-1 (0 at heads)
-          }
-          float Ssum = Sp[0] + Sp[1], dq = dqp[0] + dqp[1];
-#pragma unroll
-          for (int q = 0; q < kQ; ++q)
-            rrow[q * kRedStride] = make_float4(vals[4 * q], vals[4 * q + 1], vals[4 * q + 2], vals[4 * q + 3]);
-          Ssum += __shfl_xor_sync(0xffffffffu, Ssum, 1);
-          dq += __shfl_xor_sync(0xffffffffu, dq, 1);
-          duo[i] = fmaf(Dd, dyv, delta * Ssum);
-          ddo[i] = fmaf(ux, Ssum, dq * kLn2) * scv.w;
-          dD = fmaf(dyv, ux, dD);
-          ddtb += ddo[i];
+          for (int q = 0; q < kQ; ++q) rslot(q) = make_float4(0.f, 0.f, 0.f, 0.f);
+          duo[i] = 0.f;
+          ddo[i] = 0.f;
+          continue;
         }
-        // warp transpose-reduce of the round: lane -> (row, half, column half)
-        __syncwarp();
-        {
-          const int row = lid >> 2, rh = lid & 1, ch = (lid >> 1) & 1;
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (row < kRows) {
-            const float4* rp = &sm.red[wid][row][2 * ch + rh];
-            float4 p0 = rp[0], p1 = rp[4], p2 = rp[8], p3 = rp[12];
-            float4 p4 = rp[16], p5 = rp[20], p6 = rp[24], p7 = rp[28];
-            acc.x = ((p0.x + p1.x) + (p2.x + p3.x)) + ((p4.x + p5.x) + (p6.x + p7.x));
-            acc.y = ((p0.y + p1.y) + (p2.y + p3.y)) + ((p4.y + p5.y) + (p6.y + p7.y));
-            acc.z = ((p0.z + p1.z) + (p2.z + p3.z)) + ((p4.z + p5.z) + (p6.z + p7.z));
-            acc.w = ((p0.w + p1.w) + (p2.w + p3.w)) + ((p4.w + p5.w) + (p6.w + p7.w));
-          }
-          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
-          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
-          acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
-          acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 2);
-          if (row < kRows && ch == 0) sm.xw[sc * (kSub / 2) + round][wid][row][rh] = acc;
+        const float4 scv = sm.sc[ii][cl];
+        const float delta = scv.x, ux = scv.y, dyv = scv.z;
+        const float dux = delta * ux;
+        const bool head = sm.head[ii];
+        const float* Bt = &sm.B[ii][n0];
+        const float* Ct = &sm.C[ii][n0];
+        float Sp[2] = {0.f, 0.f}, dqp[2] = {0.f, 0.f};  // split chains
+        float vals[N];  // [dB of my NH states | dC of my NH states]
+#pragma unroll
+        for (int j = 0; j < NH; ++j) {
+          g[j] = fmaf(Ct[j], dyv, g[j]);  // g holds abar_{t+1} g_{t+1}
+          Sp[j & 1] = fmaf(g[j], Bt[j], Sp[j & 1]);
+          const float hm = head ? 0.f : fmaf(-dux, Bt[j], hb[i][j]);  // abar_t h_{t-1}
+          const float q = g[j] * hm;
+          dA[j] = fmaf(delta, q, dA[j]);
+          dqp[j & 1] = fmaf(A2[j], q, dqp[j & 1]);
+          vals[j] = g[j] * dux;
+          vals[NH + j] = dyv * hb[i][j];
+          g[j] = ab[i][j] * g[j];  // carry to t-1 (0 at heads)
         }
-        __syncwarp();
+        float Ssum = Sp[0] + Sp[1], dq = dqp[0] + dqp[1];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+          rslot(q) = make_float4(vals[4 * q], vals[4 * q + 1], vals[4 * q + 2], vals[4 * q + 3]);
+        Ssum += __shfl_xor_sync(0xffffffffu, Ssum, 1);
+        dq += __shfl_xor_sync(0xffffffffu, dq, 1);
+        duo[i] = fmaf(Dd, dyv, delta * Ssum);
+        ddo[i] = fmaf(ux, Ssum, dq * kLn2) * scv.w;
+        dD = fmaf(dyv, ux, dD);
+        ddtb += ddo[i];
       }
+      // warp transpose-reduce of the round: lane -> (row, half, column half)
+      __syncwarp();
+      {
+        const int row = lid >> 2, rh = lid & 1, ch = (lid >> 1) & 1;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < kRows) {
+          // columns 4m + (2ch + rh), m = 0..7; odd rows walk m in (m ^ 1)
+          // order so the two rows of an 8-lane phase hit disjoint banks
+          const float4* rp = &sm.red[wid][row][2 * ch + rh];
+          const int o = (row & 1) << 2;
+          float4 p0 = rp[0 ^ o], p1 = rp[4 ^ o], p2 = rp[8 ^ o], p3 = rp[12 ^ o];
+          float4 p4 = rp[16 ^ o], p5 = rp[20 ^ o], p6 = rp[24 ^ o], p7 = rp[28 ^ o];
+          acc.x = ((p0.x + p1.x) + (p2.x + p3.x)) + ((p4.x + p5.x) + (p6.x + p7.x));
+          acc.y = ((p0.y + p1.y) + (p2.y + p3.y)) + ((p4.y + p5.y) + (p6.y + p7.y));
+          acc.z = ((p0.z + p1.z) + (p2.z + p3.z)) + ((p4.z + p5.z) + (p6.z + p7.z));
+          acc.w = ((p0.w + p1.w) + (p2.w + p3.w)) + ((p4.w + p5.w) + (p6.w + p7.w));
+        }
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 2);
+        if (row < kRows && ch == 0) sm.xw[sc][wid][row][rh] = acc;
+      }
+      __syncwarp();
       if (active && hf == 0) {
         if (kFull) {
-          store4<T, kVec>(du_row, a0, a0, a0 + kSub, duo);
-          store4<T, kVec>(ddt_row, a0, a0, a0 + kSub, ddo);
+          store2<T, kVec>(du_row, a0, a0, a0 + kBSub, duo);
+          store2<T, kVec>(ddt_row, a0, a0, a0 + kBSub, ddo);
         } else {
-          store4<T, kVec>(du_row, a0, c0, c1, duo);
-          store4<T, kVec>(ddt_row, a0, c0, c1, ddo);
+          store2<T, kVec>(du_row, a0, c0, c1, duo);
+          store2<T, kVec>(ddt_row, a0, c0, c1, ddo);
         }
       }
     }
@@ -618,6 +620,12 @@ scan_bwd_kernel(const ScanBwdArgs a) {
       wsp[(int64_t)N * Dn + d] = dD;
       wsp[(int64_t)(N + 1) * Dn + d] = ddtb;
     }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (wid == 0) {
+    tmem_fence_after();
+    tmem_dealloc(sm.tmem_base, kTmemCols);
   }
 }
 
