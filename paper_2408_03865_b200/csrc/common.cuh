@@ -28,6 +28,14 @@ PM_DEV float rcp(float x) {  // MUFU.RCP
 }
 PM_DEV float sigmoidf_fast(float v) { return rcp(1.f + ex2(-v * kLog2e)); }
 
+// Packed fp32x2 arithmetic (sm_100a FFMA2/FMUL2/FADD2): two IEEE fp32
+// operations per instruction, bit-identical to the scalar ones.
+PM_DEV float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+PM_DEV float2 fmul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+PM_DEV float2 fadd2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+PM_DEV float2 f2(float v) { return make_float2(v, v); }
+PM_DEV float2 ex2x2(float2 a) { return make_float2(ex2(a.x), ex2(a.y)); }
+
 PM_DEV float lg2(float x) {  // MUFU.LG2
   float y;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -170,6 +178,34 @@ PM_DEV void store2(T* __restrict__ p, int64_t i, int64_t lo, int64_t hi, const f
       if (i + k >= lo && i + k < hi) IO<T>::st(p + i + k, v[k]);
   }
 }
+
+template <typename T, bool kVec>
+struct Raw8 {  // 8 consecutive I/O elements held raw in registers (prefetch)
+  float v[8];
+  PM_DEV void load(const T* p, int64_t i, int64_t n) { load8<T, kVec>(p, i, n, v); }
+  PM_DEV void unpack(float (&o)[8]) const {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) o[k] = v[k];
+  }
+};
+template <>
+struct Raw8<__nv_bfloat16, true> {
+  // kVec guarantees L % 8 == 0, so an 8-aligned vector is either fully inside
+  // the row or fully outside it (then it reads as zeros).
+  uint4 q;
+  PM_DEV void load(const __nv_bfloat16* p, int64_t i, int64_t n) {
+    q = (i >= 0 && i + 8 <= n) ? __ldg(reinterpret_cast<const uint4*>(p + i)) : make_uint4(0, 0, 0, 0);
+  }
+  PM_DEV void unpack(float (&o)[8]) const {
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float2 x = __bfloat1622float2(b[k]);
+      o[2 * k] = x.x;
+      o[2 * k + 1] = x.y;
+    }
+  }
+};
 
 // ------------------------------------------------------------ cp.async ----
 // 16-byte global->shared async copy (LDGSTS); src_bytes < 16 zero-fills.

@@ -12,203 +12,306 @@
 // lane-1, conv bwd needs dpre and pos from lane+1.
 // Boundary taps are SKIPPED by a predicate (o <= pos[t] && t-o >= 0), never
 // multiplied by zero.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace pm {
 
-constexpr int kConvThreads = 128;
-constexpr int kConvCh = 16;  // channels per CTA (pos reuse)
+// One warp per channel row: a warp covers kSpan = 32 lanes x 8 steps of one
+// channel per iteration (coalesced 128-bit loads/stores along L) and marches
+// through its time range; the K-1 halo comes from the neighbouring lane by
+// shuffle and is carried across iterations in registers (the paper's SRAM
+// "stagger" of reverse indices, becomes a register shuffle).  A warp
+// whose taps are all inside their sequences (every pos >= K-1: the common
+// case) runs a branch-free path; otherwise each tap is selected by the
+// predicate o <= pos[t] && t-o >= 0 (skipped, never multiplied by 0).
+constexpr int kConvWarps = 4;                  // channels per CTA
+constexpr int kConvThreads = 32 * kConvWarps;
+constexpr int kCE = 8;                         // steps per lane per iteration
+constexpr int kSpan = 32 * kCE;                // steps per warp iteration
 
-template <int K>
-struct Taps {
-  // valid[i][o] for o in [1, K-1] (o = 0 is always valid)
+template <bool kVec>
+PM_DEV void load_pos8(const int32_t* __restrict__ prow, int t0, int L, int (&p)[8]) {
+  if (kVec && t0 + 8 <= L) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(prow + t0));
+    const int4 b = __ldg(reinterpret_cast<const int4*>(prow + t0 + 4));
+    p[0] = a.x; p[1] = a.y; p[2] = a.z; p[3] = a.w;
+    p[4] = b.x; p[5] = b.y; p[6] = b.z; p[7] = b.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = (t0 + i < L) ? __ldg(prow + t0 + i) : 0;
+  }
+}
+
+// 8 consecutive position indices held in registers (prefetch)
+template <bool kVec>
+struct Pos8 {
+  int p[8];
+  PM_DEV void load(const int32_t* __restrict__ prow, int t0, int L) { load_pos8<kVec>(prow, t0, L, p); }
 };
 
+PM_DEV float silu_grad(float pre) {  // d/dpre [pre * sigmoid(pre)]
+  const float s = sigmoidf_fast(pre);
+  return s * fmaf(pre, 1.f - s, 1.f);
+}
+
 // ---------------------------------------------------------------------------
-// forward: thread = 8 time steps x kConvCh channels
+// forward
 // ---------------------------------------------------------------------------
 template <typename T, int K, bool kVec>
 __global__ void __launch_bounds__(kConvThreads)
 conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
-                const int32_t* __restrict__ pos, T* __restrict__ out, int Dn, int L, int silu) {
-  constexpr int E = 8;
-  const int r = blockIdx.z;
-  const int lid = threadIdx.x & 31;
-  const int t0 = (blockIdx.x * kConvThreads + threadIdx.x) * E;
-  const bool live = t0 < L;
-  const int32_t* pos_row = pos + (int64_t)r * L;
-
-  // tap masks: ok[i][o] <=> o <= pos[t0+i] && t0+i-o >= 0
-  bool ok[E][K];
+                const int32_t* __restrict__ pos, T* __restrict__ out, int Dn, int L, int silu,
+                int tspan) {
+  const int lid = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int d = blockIdx.x * kConvWarps + wid;
+  if (d >= Dn) return;  // warp-uniform
+  const int r = blockIdx.y;
+  const int tb = blockIdx.z * tspan, te = min(L, tb + tspan);
+  const int64_t lane = ((int64_t)r * Dn + d) * L;
+  const T* xr = x + lane;
+  T* orow = out + lane;
+  const int32_t* prow = pos + (int64_t)r * L;
+  float wk[K];
 #pragma unroll
-  for (int i = 0; i < E; ++i) {
-    const int t = t0 + i;
-    const int p = (t < L) ? __ldg(pos_row + t) : 0;
+  for (int j = 0; j < K; ++j) wk[j] = __ldg(w + (int64_t)d * K + j);
+  const float b = bias ? __ldg(bias + d) : 0.f;
+  // carry[o-1] = x[t-o] for the first step of the next iteration (lane 0)
+  float carry[K > 1 ? K - 1 : 1];
 #pragma unroll
-    for (int o = 0; o < K; ++o) ok[i][o] = (o <= p) && (t - o >= 0);
-  }
+  for (int o = 1; o < K; ++o) carry[o - 1] = (tb - o >= 0) ? IO<T>::ld(xr + tb - o) : 0.f;
 
-  const int dbase = blockIdx.y * kConvCh;
-  for (int c = 0; c < kConvCh; ++c) {
-    const int d = dbase + c;
-    if (d >= Dn) break;  // CTA-uniform
-    const int64_t lane = ((int64_t)r * Dn + d) * L;
-    float xv[E];
-    load8<T, kVec>(x + lane, t0, L, xv);
-    // halo x[t0-1 .. t0-(K-1)] from lane-1 (its last K-1 values)
-    float halo[K > 1 ? K - 1 : 1];
+  // software pipeline: the next iteration's x/pos are in flight while this
+  // one computes
+  Raw8<T, kVec> nx;
+  Pos8<kVec> np;
+  nx.load(xr, tb + lid * kCE, te);
+  np.load(prow, tb + lid * kCE, te);
+  for (int t0b = tb; t0b < te; t0b += kSpan) {
+    const int t0 = t0b + lid * kCE;
+    float xv[8];
+    int p[8];
+    nx.unpack(xv);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = np.p[i];
+    if (t0b + kSpan < te) {
+      nx.load(xr, t0 + kSpan, te);
+      np.load(prow, t0 + kSpan, te);
+    }
+    float X[K - 1 + 8];  // X[k] = x[t0 - (K-1) + k]
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      float v = __shfl_up_sync(0xffffffffu, xv[E - o], 1);
-      if (lid == 0) v = (t0 - o >= 0 && t0 - o < L) ? IO<T>::ld(x + lane + t0 - o) : 0.f;
-      halo[o - 1] = v;
+      const float v = __shfl_up_sync(0xffffffffu, xv[8 - o], 1);
+      X[K - 1 - o] = lid == 0 ? carry[o - 1] : v;
     }
-    float wk[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) wk[j] = __ldg(w + (int64_t)d * K + j);
-    const float b = bias ? __ldg(bias + d) : 0.f;
-    float yv[E];
+    for (int i = 0; i < 8; ++i) X[K - 1 + i] = xv[i];
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      float pre = b;
+    for (int o = 1; o < K; ++o) carry[o - 1] = __shfl_sync(0xffffffffu, xv[8 - o], 31);
+    bool full = t0 >= K - 1 || t0 >= te;
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const int o = K - 1 - j;
-        const float xs = (i - o >= 0) ? xv[i - o] : halo[o - i - 1];
-        if (ok[i][o]) pre = fmaf(wk[j], xs, pre);
+    for (int i = 0; i < 8; ++i) full = full && (p[i] >= K - 1 || t0 + i >= te);
+    float yv[8];
+    if (__all_sync(0xffffffffu, full)) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float pre = b;
+#pragma unroll
+        for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
+        yv[i] = silu ? pre * sigmoidf_fast(pre) : pre;
       }
-      yv[i] = silu ? pre * sigmoidf_fast(pre) : pre;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float pre = b;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int o = K - 1 - j;
+          if (o <= p[i] && t0 + i - o >= 0) pre = fmaf(wk[j], X[i + j], pre);
+        }
+        yv[i] = silu ? pre * sigmoidf_fast(pre) : pre;
+      }
     }
-    if (live) store8<T, kVec>(out + lane, t0, 0, L, yv);
+    store8<T, kVec>(orow, t0, tb, te, yv);
   }
 }
 
 // ---------------------------------------------------------------------------
-// backward: thread = 8 time steps x kConvCh channels
-//   dpre[t] = dout[t] * silu'(pre[t]);
-//   dx[s]   = sum_o [s+o < L && o <= pos[s+o]] w[K-1-o] dpre[s+o]
-//   dw[j]  += dpre[t] x[t-o] (o = K-1-j, valid tap);  db += dpre[t]
-// Per-warp partials of (dw, db) go to ws (R * nwb, Dn, K+1); a finalize
-// kernel sums them in a fixed order.
+// backward: march through the time range in REVERSE so the right halo (dpre
+// and pos of the next K-1 steps -- the "reverse indices") is always carried
+// from the previous iteration; dw/db accumulate in registers and are reduced
+// once per warp into per-(row, time-range) partials (fixed-order finalize).
 // ---------------------------------------------------------------------------
+template <typename T, int K>
+PM_DEV float dpre_at(const T* xr, const T* gr, const int32_t* prow, const float (&wk)[K], float b,
+                     int t, int L, int silu) {
+  if (t >= L) return 0.f;
+  const int pt = __ldg(prow + t);
+  float pre = b;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int o = K - 1 - j;
+    if (o <= pt && t - o >= 0) pre = fmaf(wk[j], IO<T>::ld(xr + t - o), pre);
+  }
+  return IO<T>::ld(gr + t) * (silu ? silu_grad(pre) : 1.f);
+}
+
 template <typename T, int K, bool kVec>
 __global__ void __launch_bounds__(kConvThreads)
 conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                 const int32_t* __restrict__ pos, const T* __restrict__ dout, T* __restrict__ dx,
-                float* __restrict__ ws, int Dn, int L, int silu, int nwb) {
-  constexpr int E = 8;
-  const int r = blockIdx.z;
-  const int lid = threadIdx.x & 31;
-  const int gw = (blockIdx.x * kConvThreads + threadIdx.x) >> 5;  // global warp-block in row
-  const int t0 = (blockIdx.x * kConvThreads + threadIdx.x) * E;
-  const bool live = t0 < L;
-  const int32_t* pos_row = pos + (int64_t)r * L;
-
-  // own pos and the right halo pos[t0+E .. t0+E+K-2]
-  int p[E + K - 1];
+                float* __restrict__ ws, int Dn, int L, int silu, int tspan, int ntc) {
+  const int lid = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int d = blockIdx.x * kConvWarps + wid;
+  if (d >= Dn) return;  // warp-uniform
+  const int r = blockIdx.y, tc = blockIdx.z;
+  const int tb = tc * tspan, te = min(L, tb + tspan);
+  const int64_t lane = ((int64_t)r * Dn + d) * L;
+  const T* xr = x + lane;
+  const T* gr = dout + lane;
+  T* dxr = dx + lane;
+  const int32_t* prow = pos + (int64_t)r * L;
+  float wk[K];
 #pragma unroll
-  for (int i = 0; i < E; ++i) p[i] = (t0 + i < L) ? __ldg(pos_row + t0 + i) : 0;
-#pragma unroll
-  for (int o = 1; o < K; ++o) {
-    int v = __shfl_down_sync(0xffffffffu, p[o - 1], 1);
-    const int t = t0 + E + o - 1;
-    if (lid == 31) v = (t < L) ? __ldg(pos_row + t) : 0;
-    p[E + o - 1] = v;
-  }
+  for (int j = 0; j < K; ++j) wk[j] = __ldg(w + (int64_t)d * K + j);
+  const float b = bias ? __ldg(bias + d) : 0.f;
 
-  const int dbase = blockIdx.y * kConvCh;
-  for (int c = 0; c < kConvCh; ++c) {
-    const int d = dbase + c;
-    if (d >= Dn) break;  // CTA-uniform
-    const int64_t lane = ((int64_t)r * Dn + d) * L;
-    float wk[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) wk[j] = __ldg(w + (int64_t)d * K + j);
-    const float b = bias ? __ldg(bias + d) : 0.f;
-
-    float xv[E], gv[E];
-    load8<T, kVec>(x + lane, t0, L, xv);
-    load8<T, kVec>(dout + lane, t0, L, gv);
-    float halo[K > 1 ? K - 1 : 1];  // x[t0-1 .. t0-(K-1)]
+  // right-halo carry: dpre and pos of steps te .. te+K-2 (lane o-1 computes step te+o-1)
+  float cdp[K > 1 ? K - 1 : 1];
+  int cp[K > 1 ? K - 1 : 1];
+  {
+    float myd = 0.f;
+    int myp = 0;
+    if (lid < K - 1 && te + lid < L) {
+      myd = dpre_at<T, K>(xr, gr, prow, wk, b, te + lid, L, silu);
+      myp = __ldg(prow + te + lid);
+    }
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      float v = __shfl_up_sync(0xffffffffu, xv[E - o], 1);
-      if (lid == 0) v = (t0 - o >= 0 && t0 - o < L) ? IO<T>::ld(x + lane + t0 - o) : 0.f;
-      halo[o - 1] = v;
+      cdp[o - 1] = __shfl_sync(0xffffffffu, myd, o - 1);
+      cp[o - 1] = __shfl_sync(0xffffffffu, myp, o - 1);
     }
-    // dpre for own steps
-    float dp[E + K - 1];
-    float acc_w[K], acc_b = 0.f;
+  }
+  float acc_w[K], acc_b = 0.f;
 #pragma unroll
-    for (int j = 0; j < K; ++j) acc_w[j] = 0.f;
+  for (int j = 0; j < K; ++j) acc_w[j] = 0.f;
+
+  const int nblk = (te - tb + kSpan - 1) / kSpan;
+  Raw8<T, kVec> nx, ng;
+  Pos8<kVec> np;
+  {
+    const int t0 = tb + (nblk - 1) * kSpan + lid * kCE;
+    nx.load(xr, t0, te);
+    ng.load(gr, t0, te);
+    np.load(prow, t0, te);
+  }
+  for (int blk = nblk - 1; blk >= 0; --blk) {
+    const int t0 = tb + blk * kSpan + lid * kCE;
+    float xv[8], gv[8];
+    int p[8];
+    nx.unpack(xv);
+    ng.unpack(gv);
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
+    for (int i = 0; i < 8; ++i) p[i] = np.p[i];
+    if (blk > 0) {  // prefetch the earlier block
+      nx.load(xr, t0 - kSpan, te);
+      ng.load(gr, t0 - kSpan, te);
+      np.load(prow, t0 - kSpan, te);
+    }
+    // left halo of x: lane-1 (lane 0 reads the earlier block directly)
+    float X[K - 1 + 8];
+#pragma unroll
+    for (int o = 1; o < K; ++o) {
+      const float v = __shfl_up_sync(0xffffffffu, xv[8 - o], 1);
+      X[K - 1 - o] = lid == 0 ? ((t0 - o >= 0) ? IO<T>::ld(xr + t0 - o) : 0.f) : v;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) X[K - 1 + i] = xv[i];
+    bool fullf = t0 >= K - 1 || t0 >= te;  // all forward taps valid
+#pragma unroll
+    for (int i = 0; i < 8; ++i) fullf = fullf && (p[i] >= K - 1 || t0 + i >= te);
+    const bool wfull = __all_sync(0xffffffffu, fullf);
+    // dpre for own steps; excluded taps contribute nothing to dw
+    float dp[8 + (K > 1 ? K - 1 : 0)];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
       const int t = t0 + i;
       float pre = b;
-      float xs_[K];
+      if (wfull) {
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        const int o = K - 1 - j;
-        xs_[j] = (i - o >= 0) ? xv[i - o] : halo[o - i - 1];
-        const bool okt = (o <= p[i]) && (t - o >= 0);
-        if (okt) pre = fmaf(wk[j], xs_[j], pre);
-        else xs_[j] = 0.f;  // excluded tap contributes nothing to dw
-      }
-      float gd = 1.f;
-      if (silu) {
-        const float s = sigmoidf_fast(pre);
-        gd = s * fmaf(pre, 1.f - s, 1.f);
-      }
-      const float dpv = (t < L) ? gv[i] * gd : 0.f;
-      dp[i] = dpv;
-      acc_b += dpv;
+        for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
+      } else {
 #pragma unroll
-      for (int j = 0; j < K; ++j) acc_w[j] = fmaf(dpv, xs_[j], acc_w[j]);
-    }
-    // right halo of dpre from lane+1; lane 31 recomputes it
-#pragma unroll
-    for (int o = 1; o < K; ++o) {
-      float v = __shfl_down_sync(0xffffffffu, dp[o - 1], 1);
-      if (lid == 31) {
-        const int t = t0 + E + o - 1;
-        v = 0.f;
-        if (t < L) {
-          float pre = b;
-#pragma unroll
-          for (int j = 0; j < K; ++j) {
-            const int oo = K - 1 - j;
-            if (oo <= p[E + o - 1] && t - oo >= 0) pre = fmaf(wk[j], IO<T>::ld(x + lane + t - oo), pre);
-          }
-          float gd = 1.f;
-          if (silu) {
-            const float s = sigmoidf_fast(pre);
-            gd = s * fmaf(pre, 1.f - s, 1.f);
-          }
-          v = IO<T>::ld(dout + lane + t) * gd;
+        for (int j = 0; j < K; ++j) {
+          const int o = K - 1 - j;
+          if (o <= p[i] && t - o >= 0) pre = fmaf(wk[j], X[i + j], pre);
         }
       }
-      dp[E + o - 1] = v;
-    }
-    float dxv[E];
+      const float dpv = (t < te) ? gv[i] * (silu ? silu_grad(pre) : 1.f) : 0.f;
+      dp[i] = dpv;
+      acc_b += dpv;
+      if (wfull) {
 #pragma unroll
-    for (int i = 0; i < E; ++i) {
-      float acc = 0.f;
+        for (int j = 0; j < K; ++j) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
+      } else {
 #pragma unroll
-      for (int o = 0; o < K; ++o) {
-        const int t = t0 + i + o;
-        if (t < L && o <= p[i + o]) acc = fmaf(wk[K - 1 - o], dp[i + o], acc);
+        for (int j = 0; j < K; ++j) {
+          const int o = K - 1 - j;
+          if (o <= p[i] && t - o >= 0) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
+        }
       }
-      dxv[i] = acc;
     }
-    if (live) store8<T, kVec>(dx + lane, t0, 0, L, dxv);
-    // warp reduce (dw, db) and write the per-warp partial
+    // right halo (dpre, pos of t0+8 .. t0+8+K-2) from lane+1; lane 31 uses the carry
+    int ph[K > 1 ? K - 1 : 1];
 #pragma unroll
-    for (int j = 0; j <= K; ++j) {
-      float v = j < K ? acc_w[j] : acc_b;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lid == 0 && gw < nwb) ws[(((int64_t)r * nwb + gw) * Dn + d) * (K + 1) + j] = v;
+    for (int o = 1; o < K; ++o) {
+      const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1);
+      const int vp = __shfl_down_sync(0xffffffffu, p[o - 1], 1);
+      dp[8 + o - 1] = lid == 31 ? cdp[o - 1] : vd;
+      ph[o - 1] = lid == 31 ? cp[o - 1] : vp;
     }
+    // next (earlier) iteration's carry = this block's first K-1 steps (lane 0)
+#pragma unroll
+    for (int o = 1; o < K; ++o) {
+      cdp[o - 1] = __shfl_sync(0xffffffffu, dp[o - 1], 0);
+      cp[o - 1] = __shfl_sync(0xffffffffu, p[o - 1], 0);
+    }
+    bool fullb = true;  // every dx tap valid: pos[s+o] >= o for o <= K-1, inside the row
+#pragma unroll
+    for (int o = 1; o < K; ++o) fullb = fullb && ph[o - 1] >= K - 1;
+    fullb = fullb && fullf && (t0 + 8 + K - 2 < L || t0 >= te);
+    float dxv[8];
+    if (__all_sync(0xffffffffu, fullb)) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float a = 0.f;
+#pragma unroll
+        for (int o = 0; o < K; ++o) a = fmaf(wk[K - 1 - o], dp[i + o], a);
+        dxv[i] = a;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float a = 0.f;
+#pragma unroll
+        for (int o = 0; o < K; ++o) {
+          const int t = t0 + i + o;
+          const int pt = (i + o < 8) ? p[i + o] : ph[i + o - 8];
+          if (t < L && o <= pt) a = fmaf(wk[K - 1 - o], dp[i + o], a);
+        }
+        dxv[i] = a;
+      }
+    }
+    store8<T, kVec>(dxr, t0, tb, te, dxv);
+  }
+  // one warp reduction of (dw, db) for this (row, time range, channel)
+#pragma unroll
+  for (int j = 0; j <= K; ++j) {
+    float v = j < K ? acc_w[j] : acc_b;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lid == 0) ws[(((int64_t)r * ntc + tc) * Dn + d) * (K + 1) + j] = v;
   }
 }
 
@@ -233,10 +336,18 @@ conv_bwd_finalize(const float* __restrict__ ws, float* __restrict__ dw, float* _
 namespace {
 using namespace pm;
 
-constexpr int kE = 8;
-
-int n_tblk(int64_t L) { return (int)((L + kConvThreads * kE - 1) / (kConvThreads * kE)); }
-int n_wblk(int64_t L) { return n_tblk(L) * (kConvThreads / 32); }
+// time range per CTA: whole rows when R x Dn gives enough CTAs, else split
+// (multiples of kSpan) so that ~8 waves of CTAs exist.
+int conv_tspan(int64_t R, int64_t Dn, int64_t L) {
+  const int64_t ctas = R * ((Dn + kConvWarps - 1) / kConvWarps);
+  const int64_t want = 8 * 148 * 8;
+  int64_t nt = (want + ctas - 1) / ctas;
+  const int64_t nblk = (L + kSpan - 1) / kSpan;
+  nt = std::max<int64_t>(1, std::min<int64_t>(nt, nblk));
+  const int64_t blk_per = (nblk + nt - 1) / nt;
+  return (int)(blk_per * kSpan);
+}
+int conv_ntc(int64_t L, int tspan) { return (int)((L + tspan - 1) / tspan); }
 
 bool a16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -244,7 +355,7 @@ pm_status check_conv(int64_t R, int64_t Dn, int64_t L, int32_t K, pm_dtype io) {
   if (R < 1 || Dn < 1 || L < 1) return PM_ERR_INVALID_ARG;
   if (io != PM_F32 && io != PM_BF16) return PM_ERR_DTYPE;
   if (K < 1 || K > 4) return PM_ERR_UNSUPPORTED;
-  if (R > 65535 || (Dn + kConvCh - 1) / kConvCh > 65535 || R * L >= (int64_t(1) << 31))
+  if (R > 65535 || R * L >= (int64_t(1) << 31) || (Dn + kConvWarps - 1) / kConvWarps >= (1 << 30))
     return PM_ERR_SHAPE;
   return PM_OK;
 }
@@ -257,9 +368,10 @@ bool ealigned(const void* p, pm_dtype io) {
 template <typename T, int K, bool V>
 pm_status fwd_launch(const void* x, const float* w, const float* b, const int32_t* pos, void* out,
                      int64_t R, int64_t Dn, int64_t L, int silu, cudaStream_t s) {
-  dim3 grid(n_tblk(L), (unsigned)((Dn + kConvCh - 1) / kConvCh), (unsigned)R);
+  const int tspan = conv_tspan(R, Dn, L);
+  dim3 grid((unsigned)((Dn + kConvWarps - 1) / kConvWarps), (unsigned)R, (unsigned)conv_ntc(L, tspan));
   conv_fwd_kernel<T, K, V><<<grid, kConvThreads, 0, s>>>(
-      static_cast<const T*>(x), w, b, pos, static_cast<T*>(out), (int)Dn, (int)L, silu);
+      static_cast<const T*>(x), w, b, pos, static_cast<T*>(out), (int)Dn, (int)L, silu, tspan);
   PM_LAUNCH_CHECK();
   return PM_OK;
 }
@@ -268,14 +380,14 @@ template <typename T, int K, bool V>
 pm_status bwd_launch(const void* x, const float* w, const float* b, const int32_t* pos,
                      const void* dout, void* dx, float* dw, float* db, float* ws, int64_t R,
                      int64_t Dn, int64_t L, int silu, cudaStream_t s) {
-  dim3 grid(n_tblk(L), (unsigned)((Dn + kConvCh - 1) / kConvCh), (unsigned)R);
-  const int nwb = n_wblk(L);
+  const int tspan = conv_tspan(R, Dn, L), ntc = conv_ntc(L, tspan);
+  dim3 grid((unsigned)((Dn + kConvWarps - 1) / kConvWarps), (unsigned)R, (unsigned)ntc);
   conv_bwd_kernel<T, K, V><<<grid, kConvThreads, 0, s>>>(
       static_cast<const T*>(x), w, b, pos, static_cast<const T*>(dout), static_cast<T*>(dx), ws,
-      (int)Dn, (int)L, silu, nwb);
+      (int)Dn, (int)L, silu, tspan, ntc);
   PM_LAUNCH_CHECK();
   const int64_t n = Dn * (K + 1);
-  conv_bwd_finalize<K><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, dw, db, (int)(R * nwb), (int)Dn);
+  conv_bwd_finalize<K><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, dw, db, (int)(R * ntc), (int)Dn);
   PM_LAUNCH_CHECK();
   return PM_OK;
 }
@@ -317,7 +429,7 @@ pm_status pm_causal_conv1d_fwd(const void* x, const float* w, const float* bias,
   for (const void* p : {(const void*)w, (const void*)bias, (const void*)pos})
     if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
   const int isz = io == PM_F32 ? 4 : 2;
-  const bool vec = (L * isz) % 16 == 0 && a16(x) && a16(out);
+  const bool vec = (L * isz) % 16 == 0 && L % 4 == 0 && a16(x) && a16(out) && a16(pos);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int sl = silu ? 1 : 0;
   if (io == PM_F32)
@@ -329,7 +441,7 @@ pm_status pm_causal_conv1d_fwd(const void* x, const float* w, const float* bias,
 
 size_t pm_causal_conv1d_bwd_workspace(int64_t R, int64_t Dn, int64_t L, int32_t K) {
   if (R < 1 || Dn < 1 || L < 1 || K < 1 || K > 4) return 0;
-  return (size_t)R * n_wblk(L) * Dn * (K + 1) * sizeof(float);
+  return (size_t)R * conv_ntc(L, conv_tspan(R, Dn, L)) * Dn * (K + 1) * sizeof(float);
 }
 
 pm_status pm_causal_conv1d_bwd(const void* x, const float* w, const float* bias, const int32_t* pos,
@@ -345,7 +457,7 @@ pm_status pm_causal_conv1d_bwd(const void* x, const float* w, const float* bias,
                         (const void*)dbias, (const void*)workspace})
     if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
   const int isz = io == PM_F32 ? 4 : 2;
-  const bool vec = (L * isz) % 16 == 0 && a16(x) && a16(dout) && a16(dx);
+  const bool vec = (L * isz) % 16 == 0 && L % 4 == 0 && a16(x) && a16(dout) && a16(dx) && a16(pos);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   float* ws = static_cast<float*>(workspace);
   const int sl = silu ? 1 : 0;

@@ -89,34 +89,6 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
   }
 }
 
-template <typename T, bool kVec>
-struct Raw8 {  // 8 consecutive I/O elements held raw in registers (prefetch)
-  float v[8];
-  PM_DEV void load(const T* p, int64_t i, int64_t n) { load8<T, kVec>(p, i, n, v); }
-  PM_DEV void unpack(float (&o)[8]) const {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = v[k];
-  }
-};
-template <>
-struct Raw8<__nv_bfloat16, true> {
-  // kVec guarantees L % 8 == 0, so an 8-aligned vector is either fully inside
-  // the row or fully outside it (then it reads as zeros).
-  uint4 q;
-  PM_DEV void load(const __nv_bfloat16* p, int64_t i, int64_t n) {
-    q = (i >= 0 && i + 8 <= n) ? __ldg(reinterpret_cast<const uint4*>(p + i)) : make_uint4(0, 0, 0, 0);
-  }
-  PM_DEV void unpack(float (&o)[8]) const {
-    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float2 x = __bfloat1622float2(b[k]);
-      o[2 * k] = x.x;
-      o[2 * k + 1] = x.y;
-    }
-  }
-};
-
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
@@ -146,15 +118,19 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   const T* dt_row = static_cast<const T*>(a.dt) + lane;
   T* y_row = a.y ? static_cast<T*>(a.y) + lane : nullptr;
 
-  float A2[N];
+  // states are processed in pairs with packed fp32x2 arithmetic (FFMA2)
+  constexpr int NP = N / 2;
+  float2 A2[NP];
 #pragma unroll
-  for (int n = 0; n < N; ++n) A2[n] = __ldg(a.A + (int64_t)d * N + n) * kLog2e;
+  for (int p = 0; p < NP; ++p)
+    A2[p] = make_float2(__ldg(a.A + (int64_t)d * N + 2 * p) * kLog2e,
+                        __ldg(a.A + (int64_t)d * N + 2 * p + 1) * kLog2e);
   const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
   const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
 
-  float h[N];
+  float2 h[NP];
 #pragma unroll
-  for (int n = 0; n < N; ++n) h[n] = 0.f;
+  for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
 
   // Flat loop over 8-step sub-blocks; u/dt of the next sub-block are loaded
   // into registers before the current one is computed (software pipeline),
@@ -184,7 +160,10 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     if (a.states != nullptr && (tb % kChunk) == 0 && tb >= s0 && active) {
       float* st = a.states + (((int64_t)r * a.nchunk + tb / kChunk) * N) * Dn + d;
 #pragma unroll
-      for (int n = 0; n < N; ++n) st[(int64_t)n * Dn] = h[n];
+      for (int p = 0; p < NP; ++p) {
+        st[(int64_t)(2 * p) * Dn] = h[p].x;
+        st[(int64_t)(2 * p + 1) * Dn] = h[p].y;
+      }
     }
     auto block = [&](auto full_tag) {
       constexpr bool kFull = decltype(full_tag)::value;
@@ -195,20 +174,21 @@ scan_fwd_kernel(const ScanFwdArgs a) {
         if (!kFull && (t < s0 || t >= s1)) continue;  // CTA-uniform
         const float v = vv[i] + bias;
         const float delta = a.softplus ? softplusf(v) : v;
-        const float dux = delta * uu[i];
-        const float* Bt = sB[sb + i];
-        const float* Ct = sC[sb + i];
+        const float2 dux2 = f2(delta * uu[i]), dl2 = f2(delta);
+        const float2* Bt = reinterpret_cast<const float2*>(sB[sb + i]);
+        const float2* Ct = reinterpret_cast<const float2*>(sC[sb + i]);
         if (sHead[sb + i]) {
 #pragma unroll
-          for (int n = 0; n < N; ++n) h[n] = dux * Bt[n];
+          for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
         } else {
 #pragma unroll
-          for (int n = 0; n < N; ++n) h[n] = fmaf(ex2(delta * A2[n]), h[n], dux * Bt[n]);
+          for (int p = 0; p < NP; ++p) h[p] = ffma2(ex2x2(fmul2(dl2, A2[p])), h[p], fmul2(dux2, Bt[p]));
         }
-        float yp[4] = {Dd * uu[i], 0.f, 0.f, 0.f};
+        float2 yp[2] = {make_float2(Dd * uu[i], 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int n = 0; n < N; ++n) yp[n & 3] = fmaf(Ct[n], h[n], yp[n & 3]);
-        yy[i] = (yp[0] + yp[1]) + (yp[2] + yp[3]);
+        for (int p = 0; p < NP; ++p) yp[p & 1] = ffma2(Ct[p], h[p], yp[p & 1]);
+        const float2 ys = fadd2(yp[0], yp[1]);
+        yy[i] = ys.x + ys.y;
       }
     };
     if (tb >= s0 && tb + 8 <= s1) block(std::true_type{});
@@ -371,12 +351,15 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   T* ddt_row = static_cast<T*>(a.ddt) + lane;
   float* ws_bc_r = a.ws_bc + ((int64_t)dblk * a.R + r) * (int64_t)L * (2 * N);
 
-  float A2[NH], g[NH], dA[NH];
+  // a thread's NH states are processed in pairs with packed fp32x2 (FFMA2)
+  constexpr int NP = NH / 2;
+  float2 A2[NP], g[NP], dA[NP];
 #pragma unroll
-  for (int j = 0; j < NH; ++j) {
-    A2[j] = __ldg(a.A + (int64_t)d * N + n0 + j) * kLog2e;
-    g[j] = 0.f;
-    dA[j] = 0.f;
+  for (int p = 0; p < NP; ++p) {
+    A2[p] = make_float2(__ldg(a.A + (int64_t)d * N + n0 + 2 * p) * kLog2e,
+                        __ldg(a.A + (int64_t)d * N + n0 + 2 * p + 1) * kLog2e);
+    g[p] = make_float2(0.f, 0.f);
+    dA[p] = make_float2(0.f, 0.f);
   }
   const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
   const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
@@ -390,7 +373,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     if constexpr (kVec) cp_async_wait_all();
     __syncthreads();  // raw chunk visible; previous chunk's smem readers done
     // ---- phase 1: scalars, B/C, head, chunk start state ----
-    float h[NH];
+    float2 h[NP];
     {
       float uu[8], vv[8], yy[8];
       if constexpr (kVec) {
@@ -432,20 +415,22 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         }
         if (cb > s0) {
 #pragma unroll
-          for (int j = 0; j < NH; ++j) h[j] = sm.raw.st[n0 + j][cl];
+          for (int p = 0; p < NP; ++p)
+            h[p] = make_float2(sm.raw.st[n0 + 2 * p][cl], sm.raw.st[n0 + 2 * p + 1][cl]);
         } else {
 #pragma unroll
-          for (int j = 0; j < NH; ++j) h[j] = 0.f;
+          for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
         }
       } else {
         stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.head);
         if (cb > s0) {
           const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
 #pragma unroll
-          for (int j = 0; j < NH; ++j) h[j] = st[(int64_t)j * Dn];
+          for (int p = 0; p < NP; ++p)
+            h[p] = make_float2(st[(int64_t)(2 * p) * Dn], st[(int64_t)(2 * p + 1) * Dn]);
         } else {
 #pragma unroll
-          for (int j = 0; j < NH; ++j) h[j] = 0.f;
+          for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
         }
       }
     }
@@ -460,18 +445,18 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 #pragma unroll
     for (int ii = 0; ii < kChunk; ++ii) {
       const int t = cb + ii;
-      if (ii % kBSub == 0) tmem_st<NH>(tbase + (uint32_t)((ii / kBSub) * NH), h);
+      if (ii % kBSub == 0)
+        tmem_st<NH>(tbase + (uint32_t)((ii / kBSub) * NH), reinterpret_cast<const float*>(h));
       if (!kFull && (t < c0 || t >= c1)) continue;  // CTA-uniform
       const float4 scv = sm.sc[ii][cl];
-      const float delta = scv.x;
-      const float dux = delta * scv.y;
-      const float* Bt = &sm.B[ii][n0];
+      const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
+      const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
       if (sm.head[ii]) {
 #pragma unroll
-        for (int j = 0; j < NH; ++j) h[j] = dux * Bt[j];
+        for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
       } else {
 #pragma unroll
-        for (int j = 0; j < NH; ++j) h[j] = fmaf(ex2(delta * A2[j]), h[j], dux * Bt[j]);
+        for (int p = 0; p < NP; ++p) h[p] = ffma2(ex2x2(fmul2(dl2, A2[p])), h[p], fmul2(dux2, Bt[p]));
       }
     }
 
@@ -480,35 +465,34 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     for (int sc = kBNSub - 1; sc >= 0; --sc) {
       const int a0 = cb + sc * kBSub;
       if (!kFull && (a0 >= c1 || a0 + kBSub <= c0)) continue;  // CTA-uniform
-      float hb[kBSub][NH], ab[kBSub][NH];
-      tmem_ld<NH>(tbase + (uint32_t)(sc * NH), h);
+      float2 hb[kBSub][NP], ab[kBSub][NP];
+      tmem_ld<NH>(tbase + (uint32_t)(sc * NH), reinterpret_cast<float*>(h));
 #pragma unroll
       for (int i = 0; i < kBSub; ++i) {
         const int t = a0 + i, ii = t - cb;
         if (kFull || (t >= c0 && t < c1)) {  // CTA-uniform
           const float4 scv = sm.sc[ii][cl];
-          const float delta = scv.x;
-          const float dux = delta * scv.y;
-          const float* Bt = &sm.B[ii][n0];
+          const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
+          const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
           if (sm.head[ii]) {
 #pragma unroll
-            for (int j = 0; j < NH; ++j) {
-              ab[i][j] = 0.f;
-              h[j] = dux * Bt[j];
+            for (int p = 0; p < NP; ++p) {
+              ab[i][p] = make_float2(0.f, 0.f);
+              h[p] = fmul2(dux2, Bt[p]);
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < NH; ++j) {
-              ab[i][j] = ex2(delta * A2[j]);
-              h[j] = fmaf(ab[i][j], h[j], dux * Bt[j]);
+            for (int p = 0; p < NP; ++p) {
+              ab[i][p] = ex2x2(fmul2(dl2, A2[p]));
+              h[p] = ffma2(ab[i][p], h[p], fmul2(dux2, Bt[p]));
             }
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < NH; ++j) ab[i][j] = 0.f;
+          for (int p = 0; p < NP; ++p) ab[i][p] = make_float2(0.f, 0.f);
         }
 #pragma unroll
-        for (int j = 0; j < NH; ++j) hb[i][j] = h[j];
+        for (int p = 0; p < NP; ++p) hb[i][p] = h[p];
       }
       float duo[kBSub], ddo[kBSub];
 #pragma unroll
@@ -526,27 +510,29 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         const float4 scv = sm.sc[ii][cl];
         const float delta = scv.x, ux = scv.y, dyv = scv.z;
         const float dux = delta * ux;
+        const float2 dl2 = f2(delta), dux2 = f2(dux), ndux2 = f2(-dux), dy2 = f2(dyv);
         const bool head = sm.head[ii];
-        const float* Bt = &sm.B[ii][n0];
-        const float* Ct = &sm.C[ii][n0];
-        float Sp[2] = {0.f, 0.f}, dqp[2] = {0.f, 0.f};  // split chains
-        float vals[N];  // [dB of my NH states | dC of my NH states]
+        const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
+        const float2* Ct = reinterpret_cast<const float2*>(&sm.C[ii][n0]);
+        float2 Sp = make_float2(0.f, 0.f), dqp = make_float2(0.f, 0.f);
+        float2 vals[2 * NP];  // [dB of my NH states | dC of my NH states]
 #pragma unroll
-        for (int j = 0; j < NH; ++j) {
-          g[j] = fmaf(Ct[j], dyv, g[j]);  // g holds abar_{t+1} g_{t+1}
-          Sp[j & 1] = fmaf(g[j], Bt[j], Sp[j & 1]);
-          const float hm = head ? 0.f : fmaf(-dux, Bt[j], hb[i][j]);  // abar_t h_{t-1}
-          const float q = g[j] * hm;
-          dA[j] = fmaf(delta, q, dA[j]);
-          dqp[j & 1] = fmaf(A2[j], q, dqp[j & 1]);
-          vals[j] = g[j] * dux;
-          vals[NH + j] = dyv * hb[i][j];
-          g[j] = ab[i][j] * g[j];  // carry to t-1 (0 at heads)
+        for (int p = 0; p < NP; ++p) {
+          g[p] = ffma2(Ct[p], dy2, g[p]);  // g holds abar_{t+1} g_{t+1}
+          Sp = ffma2(g[p], Bt[p], Sp);
+          // abar_t h_{t-1} = h_t - dux B  (0 at heads: post-reset abar, Q16)
+          const float2 hm = head ? make_float2(0.f, 0.f) : ffma2(ndux2, Bt[p], hb[i][p]);
+          const float2 q = fmul2(g[p], hm);
+          dA[p] = ffma2(dl2, q, dA[p]);
+          dqp = ffma2(A2[p], q, dqp);
+          vals[p] = fmul2(g[p], dux2);
+          vals[NP + p] = fmul2(dy2, hb[i][p]);
+          g[p] = fmul2(ab[i][p], g[p]);  // carry to t-1 (0 at heads)
         }
-        float Ssum = Sp[0] + Sp[1], dq = dqp[0] + dqp[1];
+        float Ssum = Sp.x + Sp.y, dq = dqp.x + dqp.y;
 #pragma unroll
         for (int q = 0; q < kQ; ++q)
-          rslot(q) = make_float4(vals[4 * q], vals[4 * q + 1], vals[4 * q + 2], vals[4 * q + 3]);
+          rslot(q) = make_float4(vals[2 * q].x, vals[2 * q].y, vals[2 * q + 1].x, vals[2 * q + 1].y);
         Ssum += __shfl_xor_sync(0xffffffffu, Ssum, 1);
         dq += __shfl_xor_sync(0xffffffffu, dq, 1);
         duo[i] = fmaf(Dd, dyv, delta * Ssum);
@@ -566,10 +552,13 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           const int o = (row & 1) << 2;
           float4 p0 = rp[0 ^ o], p1 = rp[4 ^ o], p2 = rp[8 ^ o], p3 = rp[12 ^ o];
           float4 p4 = rp[16 ^ o], p5 = rp[20 ^ o], p6 = rp[24 ^ o], p7 = rp[28 ^ o];
-          acc.x = ((p0.x + p1.x) + (p2.x + p3.x)) + ((p4.x + p5.x) + (p6.x + p7.x));
-          acc.y = ((p0.y + p1.y) + (p2.y + p3.y)) + ((p4.y + p5.y) + (p6.y + p7.y));
-          acc.z = ((p0.z + p1.z) + (p2.z + p3.z)) + ((p4.z + p5.z) + (p6.z + p7.z));
-          acc.w = ((p0.w + p1.w) + (p2.w + p3.w)) + ((p4.w + p5.w) + (p6.w + p7.w));
+          auto lo = [](float4 v) { return make_float2(v.x, v.y); };
+          auto hi = [](float4 v) { return make_float2(v.z, v.w); };
+          const float2 sl = fadd2(fadd2(fadd2(lo(p0), lo(p1)), fadd2(lo(p2), lo(p3))),
+                                  fadd2(fadd2(lo(p4), lo(p5)), fadd2(lo(p6), lo(p7))));
+          const float2 sh = fadd2(fadd2(fadd2(hi(p0), hi(p1)), fadd2(hi(p2), hi(p3))),
+                                  fadd2(fadd2(hi(p4), hi(p5)), fadd2(hi(p6), hi(p7))));
+          acc = make_float4(sl.x, sl.y, sh.x, sh.y);
         }
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
@@ -615,7 +604,10 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   }
   if (active) {
 #pragma unroll
-    for (int j = 0; j < NH; ++j) wsp[(int64_t)(n0 + j) * Dn + d] = dA[j];
+    for (int p = 0; p < NP; ++p) {
+      wsp[(int64_t)(n0 + 2 * p) * Dn + d] = dA[p].x;
+      wsp[(int64_t)(n0 + 2 * p + 1) * Dn + d] = dA[p].y;
+    }
     if (hf == 0) {
       wsp[(int64_t)N * Dn + d] = dD;
       wsp[(int64_t)(N + 1) * Dn + d] = ddtb;
