@@ -20,6 +20,7 @@
 //    shared memory, then over warps, into per-channel-block partials that a
 //    finalize kernel sums in a fixed order (deterministic).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -32,6 +33,8 @@ constexpr int kTile = 64;   // fwd staging tile (time steps)
 constexpr int kChunk = 16;  // checkpoint interval (time steps)
 constexpr int kSub = 4;     // bwd register sub-chunk (time steps)
 constexpr int kNSub = kChunk / kSub;
+constexpr int kFwdMinB = 4;  // resident fwd CTAs per SM (register cap 128)
+constexpr int kBwdMinB = 4;  // resident bwd CTAs per SM (register cap 128; smem fits 4)
 
 struct ScanFwdArgs {
   const void* u;
@@ -92,8 +95,8 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
-template <typename T, int N, bool kVec>
-__global__ void __launch_bounds__(kScanThreads, 4)
+template <typename T, int N, bool kVec, int MinB>
+__global__ void __launch_bounds__(kScanThreads, MinB)
 scan_fwd_kernel(const ScanFwdArgs a) {
   __shared__ __align__(16) float sB[kTile][N];
   __shared__ __align__(16) float sC[kTile][N];
@@ -300,8 +303,8 @@ PM_DEV void bwd_issue_raw(BwdRaw<T, N>& rw, const ScanBwdArgs& a, int r, int dbl
   cp_async_commit();
 }
 
-template <typename T, int N, bool kVec>
-__global__ void __launch_bounds__(kBwdThreads, 4)
+template <typename T, int N, bool kVec, int MinB>
+__global__ void __launch_bounds__(kBwdThreads, MinB)
 scan_bwd_kernel(const ScanBwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using SM = BwdSmem<T, N>;
@@ -442,12 +445,11 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     auto passes = [&](auto full_tag) {
       constexpr bool kFull = decltype(full_tag)::value;
     // ---- pass A: forward over the chunk, record sub-chunk start states ----
-#pragma unroll
-    for (int ii = 0; ii < kChunk; ++ii) {
+    auto stepA = [&](const int ii) {
       const int t = cb + ii;
       if (ii % kBSub == 0)
         tmem_st<NH>(tbase + (uint32_t)((ii / kBSub) * NH), reinterpret_cast<const float*>(h));
-      if (!kFull && (t < c0 || t >= c1)) continue;  // CTA-uniform
+      if (!kFull && (t < c0 || t >= c1)) return;  // CTA-uniform
       const float4 scv = sm.sc[ii][cl];
       const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
       const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
@@ -458,13 +460,21 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) h[p] = ffma2(ex2x2(fmul2(dl2, A2[p])), h[p], fmul2(dux2, Bt[p]));
       }
+    };
+    if constexpr (kFull) {
+#pragma unroll
+      for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
+    } else {
+#pragma unroll 1
+      for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
     }
-
     tmem_wait_st();  // sub-chunk states are in TMEM before pass B reads them
-    // ---- pass B: 2-step sub-chunks in reverse (= one reduction round) ----
-    for (int sc = kBNSub - 1; sc >= 0; --sc) {
+    // ---- pass B: 2-step sub-chunks in reverse (= one reduction round);
+    //      fully unrolled on the full-chunk path so every shared-memory and
+    //      TMEM offset is an immediate ----
+    auto sub_chunk = [&](const int sc) {
       const int a0 = cb + sc * kBSub;
-      if (!kFull && (a0 >= c1 || a0 + kBSub <= c0)) continue;  // CTA-uniform
+      if (!kFull && (a0 >= c1 || a0 + kBSub <= c0)) return;  // CTA-uniform
       float2 hb[kBSub][NP], ab[kBSub][NP];
       tmem_ld<NH>(tbase + (uint32_t)(sc * NH), reinterpret_cast<float*>(h));
 #pragma unroll
@@ -478,21 +488,22 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
               ab[i][p] = make_float2(0.f, 0.f);
-              h[p] = fmul2(dux2, Bt[p]);
+              hb[i][p] = fmul2(dux2, Bt[p]);
             }
           } else {
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
               ab[i][p] = ex2x2(fmul2(dl2, A2[p]));
-              h[p] = ffma2(ab[i][p], h[p], fmul2(dux2, Bt[p]));
+              hb[i][p] = ffma2(ab[i][p], i == 0 ? h[p] : hb[i - 1][p], fmul2(dux2, Bt[p]));
             }
           }
         } else {
 #pragma unroll
-          for (int p = 0; p < NP; ++p) ab[i][p] = make_float2(0.f, 0.f);
+          for (int p = 0; p < NP; ++p) {
+            ab[i][p] = make_float2(0.f, 0.f);
+            hb[i][p] = i == 0 ? h[p] : hb[i - 1][p];
+          }
         }
-#pragma unroll
-        for (int p = 0; p < NP; ++p) hb[i][p] = h[p];
       }
       float duo[kBSub], ddo[kBSub];
 #pragma unroll
@@ -576,6 +587,13 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           store2<T, kVec>(ddt_row, a0, c0, c1, ddo);
         }
       }
+    };
+    if constexpr (kFull) {
+#pragma unroll 2
+      for (int sc = kBNSub - 1; sc >= 0; --sc) sub_chunk(sc);
+    } else {
+#pragma unroll 1
+      for (int sc = kBNSub - 1; sc >= 0; --sc) sub_chunk(sc);
     }
     };
     if (c0 == cb && c1 == cb + kChunk) passes(std::true_type{});
@@ -704,10 +722,23 @@ bool elem_aligned(const void* p, pm_dtype io) {
   return p == nullptr || (reinterpret_cast<uintptr_t>(p) & m) == 0;
 }
 
+// Occupancy variants (min resident CTAs per SM -> register cap).  The
+// default is the measured best on B200; PM_TUNE_FWD_MINB / PM_TUNE_BWD_MINB
+// override it for tuning sweeps (read per call; no global state).
+int tune_env(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
 template <typename T, int N, bool kVec>
 pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
   dim3 grid(n_dblk(a.Dn), a.R, a.nseg);
-  scan_fwd_kernel<T, N, kVec><<<grid, kScanThreads, 0, s>>>(a);
+  switch (tune_env("PM_TUNE_FWD_MINB", kFwdMinB)) {
+    case 3: scan_fwd_kernel<T, N, kVec, 3><<<grid, kScanThreads, 0, s>>>(a); break;
+    case 5: scan_fwd_kernel<T, N, kVec, 5><<<grid, kScanThreads, 0, s>>>(a); break;
+    case 6: scan_fwd_kernel<T, N, kVec, 6><<<grid, kScanThreads, 0, s>>>(a); break;
+    default: scan_fwd_kernel<T, N, kVec, 4><<<grid, kScanThreads, 0, s>>>(a); break;
+  }
   PM_LAUNCH_CHECK();
   return PM_OK;
 }
@@ -730,7 +761,8 @@ template <typename T, int N, bool kVec>
 pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, float* dD,
                      float* ddtb, cudaStream_t s) {
   const size_t smem = sizeof(BwdSmem<T, N>);
-  auto kern = scan_bwd_kernel<T, N, kVec>;
+  auto kern = tune_env("PM_TUNE_BWD_MINB", kBwdMinB) == 3 ? scan_bwd_kernel<T, N, kVec, 3>
+                                                          : scan_bwd_kernel<T, N, kVec, 4>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return PM_ERR_CUDA;
   dim3 grid(n_dblk_bwd(a.Dn), a.R, a.nseg);
