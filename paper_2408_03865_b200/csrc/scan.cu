@@ -73,7 +73,7 @@ struct ScanBwdArgs {
 template <typename T, int N, int W, bool kVec>
 PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
                      const int32_t* __restrict__ pos_row, int L, int j0,
-                     float (*sB)[N], float (*sC)[N], int* sHead) {
+                     float (*sB)[N], float (*sC)[N], unsigned* sMask) {
   static_assert(W % 8 == 0, "window must be a multiple of 8");
   for (int e = threadIdx.x; e < N * (W / 8); e += blockDim.x) {
     const int n = e % N, tb = (e / N) * 8;
@@ -86,9 +86,15 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
       sC[tb + i][n] = vc[i];
     }
   }
-  for (int e = threadIdx.x; e < W; e += blockDim.x) {
-    const int t = j0 + e;
-    sHead[e] = (t >= L) ? 1 : (t == 0 || __ldg(pos_row + t) == 0);
+  // head flags of the window as a bitmask (warp 0 ballots 32 steps at a time)
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int w0 = 0; w0 < W; w0 += 32) {
+      const int t = j0 + w0 + (int)threadIdx.x;
+      const bool f = (w0 + (int)threadIdx.x < W) && ((t >= L) || t == 0 || __ldg(pos_row + t) == 0);
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (threadIdx.x == 0) sMask[w0 / 32] = m;
+    }
   }
 }
 
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(kScanThreads, MinB)
 scan_fwd_kernel(const ScanFwdArgs a) {
   __shared__ __align__(16) float sB[kTile][N];
   __shared__ __align__(16) float sC[kTile][N];
-  __shared__ int sHead[kTile];
+  __shared__ unsigned sMask[kTile / 32];
   __shared__ int s_red[kScanWarps];
 
   const int r = blockIdx.y, k = blockIdx.z;
@@ -144,12 +150,16 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   pu.load(u_row, tb, L);
   pt.load(dt_row, tb, L);
   int j0 = -1;
+  unsigned long long hmask = 0ull;
   for (; tb < s1; tb += 8) {
     if (j0 < 0 || (tb & (kTile - 1)) == 0) {  // CTA-uniform
       j0 = tb & ~(kTile - 1);
       __syncthreads();
-      stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sHead);
+      stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask);
       __syncthreads();
+      // head flags of the tile as a register bitmask (CTA-uniform): no
+      // shared-memory load on the per-step critical path
+      hmask = (unsigned long long)sMask[0] | ((unsigned long long)sMask[1] << 32);
     }
     float uu[8], vv[8], yy[8];
     pu.unpack(uu);
@@ -180,7 +190,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
         const float2 dux2 = f2(delta * uu[i]), dl2 = f2(delta);
         const float2* Bt = reinterpret_cast<const float2*>(sB[sb + i]);
         const float2* Ct = reinterpret_cast<const float2*>(sC[sb + i]);
-        if (sHead[sb + i]) {
+        if ((hmask >> (sb + i)) & 1ull) {
 #pragma unroll
           for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
         } else {
@@ -253,7 +263,7 @@ struct BwdSmem {
   float4 xw[kChunk / 2][kBwdWarps][kRows][2];
   float B[kChunk][N];
   float C[kChunk][N];
-  int head[kChunk];
+  unsigned hmask[1];  // head flags of the chunk (bit e = step cb + e)
   int s_red[kBwdWarps];
   uint32_t tmem_base;
 };
@@ -412,9 +422,11 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           sm.B[t][n] = IO<T>::cvt(sm.raw.B[n][t]);
           sm.C[t][n] = IO<T>::cvt(sm.raw.C[n][t]);
         }
-        for (int e = tid; e < kChunk; e += kBwdThreads) {
-          const int t = cb + e;
-          sm.head[e] = (t >= L) ? 1 : (t == 0 || sm.raw.pos[e] == 0);
+        if (tid < 32) {
+          const int t = cb + tid;
+          const bool f = tid < kChunk && (t >= L || t == 0 || sm.raw.pos[tid & (kChunk - 1)] == 0);
+          const unsigned m = __ballot_sync(0xffffffffu, f);
+          if (tid == 0) sm.hmask[0] = m;
         }
         if (cb > s0) {
 #pragma unroll
@@ -425,7 +437,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
         }
       } else {
-        stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.head);
+        stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.hmask);
         if (cb > s0) {
           const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
 #pragma unroll
@@ -438,6 +450,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
       }
     }
     __syncthreads();  // scalars visible; raw buffer free
+    const uint32_t hmask = sm.hmask[0];  // head flags of the chunk (CTA-uniform register)
     if constexpr (kVec) {
       if (c > cfirst) bwd_issue_raw<T, N>(sm.raw, a, r, dblk, c - 1, s0);
     }
@@ -453,7 +466,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
       const float4 scv = sm.sc[ii][cl];
       const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
       const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
-      if (sm.head[ii]) {
+      if ((hmask >> ii) & 1u) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
       } else {
@@ -484,7 +497,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           const float4 scv = sm.sc[ii][cl];
           const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
           const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
-          if (sm.head[ii]) {
+          if ((hmask >> ii) & 1u) {
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
               ab[i][p] = make_float2(0.f, 0.f);
@@ -522,7 +535,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         const float delta = scv.x, ux = scv.y, dyv = scv.z;
         const float dux = delta * ux;
         const float2 dl2 = f2(delta), dux2 = f2(dux), ndux2 = f2(-dux), dy2 = f2(dyv);
-        const bool head = sm.head[ii];
+        const bool head = (hmask >> ii) & 1u;
         const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
         const float2* Ct = reinterpret_cast<const float2*>(&sm.C[ii][n0]);
         float2 Sp = make_float2(0.f, 0.f), dqp = make_float2(0.f, 0.f);
