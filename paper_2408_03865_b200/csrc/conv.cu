@@ -59,11 +59,10 @@ PM_DEV float silu_grad(float pre) {  // d/dpre [pre * sigmoid(pre)]
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
-template <typename T, int K, bool kVec>
+template <typename T, int K, bool kVec, bool kSilu>
 __global__ void __launch_bounds__(kConvThreads)
 conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
-                const int32_t* __restrict__ pos, T* __restrict__ out, int Dn, int L, int silu,
-                int tspan) {
+                const int32_t* __restrict__ pos, T* __restrict__ out, int Dn, int L, int tspan) {
   const int lid = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int d = blockIdx.x * kConvWarps + wid;
   if (d >= Dn) return;  // warp-uniform
@@ -119,7 +118,7 @@ conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
         float pre = b;
 #pragma unroll
         for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
-        yv[i] = silu ? pre * sigmoidf_fast(pre) : pre;
+        yv[i] = kSilu ? pre * sigmoidf_fast(pre) : pre;
       }
     } else {
 #pragma unroll
@@ -130,7 +129,7 @@ conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
           const int o = K - 1 - j;
           if (o <= p[i] && t0 + i - o >= 0) pre = fmaf(wk[j], X[i + j], pre);
         }
-        yv[i] = silu ? pre * sigmoidf_fast(pre) : pre;
+        yv[i] = kSilu ? pre * sigmoidf_fast(pre) : pre;
       }
     }
     store8<T, kVec>(orow, t0, tb, te, yv);
@@ -157,11 +156,11 @@ PM_DEV float dpre_at(const T* xr, const T* gr, const int32_t* prow, const float 
   return IO<T>::ld(gr + t) * (silu ? silu_grad(pre) : 1.f);
 }
 
-template <typename T, int K, bool kVec>
+template <typename T, int K, bool kVec, bool kSilu>
 __global__ void __launch_bounds__(kConvThreads)
 conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                 const int32_t* __restrict__ pos, const T* __restrict__ dout, T* __restrict__ dx,
-                float* __restrict__ ws, int Dn, int L, int silu, int tspan, int ntc) {
+                float* __restrict__ ws, int Dn, int L, int tspan, int ntc) {
   const int lid = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int d = blockIdx.x * kConvWarps + wid;
   if (d >= Dn) return;  // warp-uniform
@@ -176,15 +175,16 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
 #pragma unroll
   for (int j = 0; j < K; ++j) wk[j] = __ldg(w + (int64_t)d * K + j);
   const float b = bias ? __ldg(bias + d) : 0.f;
+  constexpr int H = K > 1 ? K - 1 : 1;
 
   // right-halo carry: dpre and pos of steps te .. te+K-2 (lane o-1 computes step te+o-1)
-  float cdp[K > 1 ? K - 1 : 1];
-  int cp[K > 1 ? K - 1 : 1];
+  float cdp[H];
+  int cp[H];
   {
     float myd = 0.f;
     int myp = 0;
     if (lid < K - 1 && te + lid < L) {
-      myd = dpre_at<T, K>(xr, gr, prow, wk, b, te + lid, L, silu);
+      myd = dpre_at<T, K>(xr, gr, prow, wk, b, te + lid, L, kSilu ? 1 : 0);
       myp = __ldg(prow + te + lid);
     }
 #pragma unroll
@@ -228,61 +228,40 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) X[K - 1 + i] = xv[i];
-    bool fullf = t0 >= K - 1 || t0 >= te;  // all forward taps valid
-#pragma unroll
-    for (int i = 0; i < 8; ++i) fullf = fullf && (p[i] >= K - 1 || t0 + i >= te);
-    const bool wfull = __all_sync(0xffffffffu, fullf);
-    // dpre for own steps; excluded taps contribute nothing to dw
-    float dp[8 + (K > 1 ? K - 1 : 0)];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int t = t0 + i;
-      float pre = b;
-      if (wfull) {
-#pragma unroll
-        for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
-      } else {
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int o = K - 1 - j;
-          if (o <= p[i] && t - o >= 0) pre = fmaf(wk[j], X[i + j], pre);
-        }
-      }
-      const float dpv = (t < te) ? gv[i] * (silu ? silu_grad(pre) : 1.f) : 0.f;
-      dp[i] = dpv;
-      acc_b += dpv;
-      if (wfull) {
-#pragma unroll
-        for (int j = 0; j < K; ++j) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int o = K - 1 - j;
-          if (o <= p[i] && t - o >= 0) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
-        }
-      }
-    }
-    // right halo (dpre, pos of t0+8 .. t0+8+K-2) from lane+1; lane 31 uses the carry
-    int ph[K > 1 ? K - 1 : 1];
+    // right halo of pos from lane+1 (lane 31: carry)
+    int ph[H];
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1);
       const int vp = __shfl_down_sync(0xffffffffu, p[o - 1], 1);
-      dp[8 + o - 1] = lid == 31 ? cdp[o - 1] : vd;
       ph[o - 1] = lid == 31 ? cp[o - 1] : vp;
     }
-    // next (earlier) iteration's carry = this block's first K-1 steps (lane 0)
+    // one decision per iteration: every forward tap and every dx tap valid,
+    // all 8 steps inside the range (the common case), else per-tap predicates
+    bool full = t0 >= K - 1 && t0 + 8 <= te && t0 + 8 + K - 2 < L;
 #pragma unroll
-    for (int o = 1; o < K; ++o) {
-      cdp[o - 1] = __shfl_sync(0xffffffffu, dp[o - 1], 0);
-      cp[o - 1] = __shfl_sync(0xffffffffu, p[o - 1], 0);
-    }
-    bool fullb = true;  // every dx tap valid: pos[s+o] >= o for o <= K-1, inside the row
+    for (int i = 0; i < 8; ++i) full = full && p[i] >= K - 1;
 #pragma unroll
-    for (int o = 1; o < K; ++o) fullb = fullb && ph[o - 1] >= K - 1;
-    fullb = fullb && fullf && (t0 + 8 + K - 2 < L || t0 >= te);
+    for (int o = 1; o < K; ++o) full = full && ph[o - 1] >= K - 1;
+    const bool wfull = __all_sync(0xffffffffu, full);
+    float dp[8 + H];
     float dxv[8];
-    if (__all_sync(0xffffffffu, fullb)) {
+    if (wfull) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float pre = b;
+#pragma unroll
+        for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
+        const float dpv = gv[i] * (kSilu ? silu_grad(pre) : 1.f);
+        dp[i] = dpv;
+        acc_b += dpv;
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
+      }
+#pragma unroll
+      for (int o = 1; o < K; ++o) {
+        const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1);
+        dp[8 + o - 1] = lid == 31 ? cdp[o - 1] : vd;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float a = 0.f;
@@ -291,6 +270,29 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
         dxv[i] = a;
       }
     } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int t = t0 + i;
+        float pre = b;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int o = K - 1 - j;
+          if (o <= p[i] && t - o >= 0) pre = fmaf(wk[j], X[i + j], pre);
+        }
+        const float dpv = (t < te) ? gv[i] * (kSilu ? silu_grad(pre) : 1.f) : 0.f;
+        dp[i] = dpv;
+        acc_b += dpv;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int o = K - 1 - j;
+          if (o <= p[i] && t - o >= 0) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
+        }
+      }
+#pragma unroll
+      for (int o = 1; o < K; ++o) {
+        const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1);
+        dp[8 + o - 1] = lid == 31 ? cdp[o - 1] : vd;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float a = 0.f;
@@ -302,6 +304,12 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
         }
         dxv[i] = a;
       }
+    }
+    // next (earlier) iteration's carry = this block's first K-1 steps (lane 0)
+#pragma unroll
+    for (int o = 1; o < K; ++o) {
+      cdp[o - 1] = __shfl_sync(0xffffffffu, dp[o - 1], 0);
+      cp[o - 1] = __shfl_sync(0xffffffffu, p[o - 1], 0);
     }
     store8<T, kVec>(dxr, t0, tb, te, dxv);
   }
@@ -370,8 +378,12 @@ pm_status fwd_launch(const void* x, const float* w, const float* b, const int32_
                      int64_t R, int64_t Dn, int64_t L, int silu, cudaStream_t s) {
   const int tspan = conv_tspan(R, Dn, L);
   dim3 grid((unsigned)((Dn + kConvWarps - 1) / kConvWarps), (unsigned)R, (unsigned)conv_ntc(L, tspan));
-  conv_fwd_kernel<T, K, V><<<grid, kConvThreads, 0, s>>>(
-      static_cast<const T*>(x), w, b, pos, static_cast<T*>(out), (int)Dn, (int)L, silu, tspan);
+  if (silu)
+    conv_fwd_kernel<T, K, V, true><<<grid, kConvThreads, 0, s>>>(
+        static_cast<const T*>(x), w, b, pos, static_cast<T*>(out), (int)Dn, (int)L, tspan);
+  else
+    conv_fwd_kernel<T, K, V, false><<<grid, kConvThreads, 0, s>>>(
+        static_cast<const T*>(x), w, b, pos, static_cast<T*>(out), (int)Dn, (int)L, tspan);
   PM_LAUNCH_CHECK();
   return PM_OK;
 }
@@ -382,9 +394,14 @@ pm_status bwd_launch(const void* x, const float* w, const float* b, const int32_
                      int64_t Dn, int64_t L, int silu, cudaStream_t s) {
   const int tspan = conv_tspan(R, Dn, L), ntc = conv_ntc(L, tspan);
   dim3 grid((unsigned)((Dn + kConvWarps - 1) / kConvWarps), (unsigned)R, (unsigned)ntc);
-  conv_bwd_kernel<T, K, V><<<grid, kConvThreads, 0, s>>>(
-      static_cast<const T*>(x), w, b, pos, static_cast<const T*>(dout), static_cast<T*>(dx), ws,
-      (int)Dn, (int)L, silu, tspan, ntc);
+  if (silu)
+    conv_bwd_kernel<T, K, V, true><<<grid, kConvThreads, 0, s>>>(
+        static_cast<const T*>(x), w, b, pos, static_cast<const T*>(dout), static_cast<T*>(dx), ws,
+        (int)Dn, (int)L, tspan, ntc);
+  else
+    conv_bwd_kernel<T, K, V, false><<<grid, kConvThreads, 0, s>>>(
+        static_cast<const T*>(x), w, b, pos, static_cast<const T*>(dout), static_cast<T*>(dx), ws,
+        (int)Dn, (int)L, tspan, ntc);
   PM_LAUNCH_CHECK();
   const int64_t n = Dn * (K + 1);
   conv_bwd_finalize<K><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(ws, dw, db, (int)(R * ntc), (int)Dn);
