@@ -174,10 +174,13 @@ PM_API pm_status pm_causal_conv1d_bwd(const void* x, const float* w,
  *   y[r,d,t] = sum_n C[r,n,t]*h_n + Dskip[d]*u[r,d,t] (Eq 1b + skip, Q3)
  * The reset makes the recurrence a segmented associative scan.
  *   Dskip, dt_bias may be NULL (0).
- *   states (optional, may be NULL): pm_selective_scan_state_bytes() bytes of
- *     fp32 chunk-boundary states written for the backward pass ("reused
- *     Mamba's structure for handling hidden_state").  Layout is
- *     private to the library; pass the same buffer to the backward pass. */
+ *   states (optional, may be NULL): pm_selective_scan_state_bytes() bytes,
+ *     16-byte aligned: the fp32 chunk-boundary states written for the
+ *     backward pass ("reused Mamba's structure for handling hidden_state",
+ *     P:234) plus the length-sorted segment schedule that lets both passes
+ *     run persistent, longest-first.  Layout is private to the library; pass
+ *     the same buffer to the backward pass.  With states == NULL the forward
+ *     runs a plain grid (no schedule). */
 PM_API size_t pm_selective_scan_state_bytes(int64_t R, int64_t Dn, int64_t L,
                                      int32_t N);
 PM_API pm_status pm_selective_scan_fwd(const void* u, const void* dt,

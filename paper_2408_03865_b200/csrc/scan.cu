@@ -21,6 +21,7 @@
 //    finalize kernel sums in a fixed order (deterministic).
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <type_traits>
 
 #include "common.cuh"
@@ -47,6 +48,9 @@ struct ScanFwdArgs {
   const int32_t* pos;
   void* y;
   float* states;
+  const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
+  int* counter;       // work counter for the persistent loop
+  int n_items;
   int R, Dn, L, nseg, nchunk, softplus;
 };
 
@@ -65,7 +69,68 @@ struct ScanBwdArgs {
   void* ddt;
   float* ws_bc;     // (nDblk, R, L, 2N)
   float* ws_param;  // (R*nseg, N+2, Dn)
+  const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
+  int* counter;
+  int n_items;
   int R, Dn, L, nseg, nchunk, softplus;
+};
+
+// ---------------------------------------------------------------------------
+// Work scheduling.  Segment lengths follow the sequence-length distribution
+// (57..2048 steps), so a plain grid leaves a long tail.  A planning kernel
+// lists every row's segments, one CTA sorts them longest-first, and the scan
+// kernels are persistent: each CTA pulls (segment, channel-block) items from
+// an atomic counter in that order (LPT), so the last items are the shortest.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) seg_plan_kernel(const int32_t* __restrict__ pos, int L,
+                                                      int nseg, int4* __restrict__ items) {
+  // cut k (1 <= k < nseg) = first head at or after k * ceil(L / nseg), as in
+  // segment_bounds(); one warp per cut, 32 positions per ballot
+  __shared__ int cut[65];
+  const int r = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t* pos_row = pos + (int64_t)r * L;
+  const int seg = (L + nseg - 1) / nseg;
+  for (int k = 1 + warp; k < nseg; k += blockDim.x >> 5) {
+    int b = L;
+    for (int base = k * seg; base < L; base += 32) {
+      const int t = base + lane;
+      const unsigned m = __ballot_sync(0xffffffffu, t < L && __ldg(pos_row + t) == 0);
+      if (m) {
+        b = base + __ffs(m) - 1;
+        break;
+      }
+    }
+    if (lane == 0) cut[k] = min(b, L);
+  }
+  if (threadIdx.x == 0) {
+    cut[0] = 0;
+    cut[nseg] = L;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nseg; k += blockDim.x)
+    items[r * nseg + k] = make_int4(r, k, cut[k], max(cut[k], cut[k + 1]));
+}
+
+// rank sort by length (descending), ties by index: O(n^2 / threads)
+__global__ void __launch_bounds__(1024) seg_sort_kernel(const int4* __restrict__ in, int n,
+                                                       int4* __restrict__ out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int4 a = in[i];
+    const int la = a.w - a.z;
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const int4 b = in[j];
+      const int lb = b.w - b.z;
+      rank += (lb > la) || (lb == la && j < i);
+    }
+    out[rank] = a;
+  }
+}
+
+// next work item: persistent (sorted list + counter) or grid mode (1 item)
+struct Work {
+  int r, k, dblk, s0, s1;
+  bool valid;
 };
 
 // Stage B, C (converted to fp32, time-major [t][n]) and head flags for the
@@ -108,17 +173,34 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   __shared__ __align__(16) float sC[kTile][N];
   __shared__ unsigned sMask[kTile / 32];
   __shared__ int s_red[kScanWarps];
+  __shared__ int s_work;
 
-  const int r = blockIdx.y, k = blockIdx.z;
   const int L = a.L, Dn = a.Dn;
-  const int d_raw = blockIdx.x * kScanThreads + threadIdx.x;
+  const int ndblk = (Dn + kScanThreads - 1) / kScanThreads;
+  for (int iter = 0;; ++iter) {
+  int r, dblk, s0, s1;
+  if (a.items != nullptr) {  // persistent: longest segments first
+    __syncthreads();
+    if (threadIdx.x == 0) s_work = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int w = s_work;
+    if (w >= a.n_items * ndblk) break;
+    const int4 it = a.items[w / ndblk];
+    r = it.x;
+    dblk = w % ndblk;
+    s0 = it.z;
+    s1 = it.w;
+  } else {
+    if (iter > 0) break;
+    r = blockIdx.y;
+    dblk = blockIdx.x;
+    segment_bounds(a.pos + (int64_t)r * L, L, blockIdx.z, a.nseg, s_red, s0, s1);
+  }
+  if (s0 >= s1) continue;
+  const int d_raw = dblk * kScanThreads + threadIdx.x;
   const bool active = d_raw < Dn;
   const int d = active ? d_raw : Dn - 1;
   const int32_t* pos_row = a.pos + (int64_t)r * L;
-
-  int s0, s1;
-  segment_bounds(pos_row, L, k, a.nseg, s_red, s0, s1);
-  if (s0 >= s1) return;
 
   const T* B_r = static_cast<const T*>(a.B) + (int64_t)r * N * L;
   const T* C_r = static_cast<const T*>(a.C) + (int64_t)r * N * L;
@@ -208,6 +290,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     else block(std::false_type{});
     if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
   }
+  }  // work loop
 }
 
 // ---------------------------------------------------------------------------
@@ -321,19 +404,47 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   constexpr int NH = SM::NH, kQ = SM::kQ, kRows = SM::kRows;
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
-  const int r = blockIdx.y, k = blockIdx.z, dblk = blockIdx.x;
   const int L = a.L, Dn = a.Dn;
   const int tid = threadIdx.x, lid = tid & 31, wid = tid >> 5;
   const int cl = tid >> 1, hf = tid & 1;
+  const int n0 = hf * NH;  // first state of this thread
+  const int ndblk = (Dn + kBwdCh - 1) / kBwdCh;
+  // sub-chunk start states live in tensor memory (one TMEM lane per thread,
+  // kBNSub * NH fp32 columns), freeing shared memory for a 4th CTA per SM.
+  constexpr uint32_t kTmemCols = (kBNSub * NH <= 32) ? 32u : (kBNSub * NH <= 64 ? 64u : 128u);
+  if (wid == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = sm.tmem_base + ((uint32_t)((wid & 3) * 32) << 16);
+
+  for (int iter = 0;; ++iter) {
+  int r, k, dblk, s0, s1;
+  if (a.items != nullptr) {  // persistent: longest segments first
+    __syncthreads();
+    if (tid == 0) sm.s_red[0] = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int w = sm.s_red[0];
+    __syncthreads();
+    if (w >= a.n_items * ndblk) break;
+    const int4 it = a.items[w / ndblk];
+    r = it.x;
+    k = it.y;
+    dblk = w % ndblk;
+    s0 = it.z;
+    s1 = it.w;
+  } else {
+    if (iter > 0) break;
+    r = blockIdx.y;
+    k = blockIdx.z;
+    dblk = blockIdx.x;
+    segment_bounds(a.pos + (int64_t)r * L, L, k, a.nseg, sm.s_red, s0, s1);
+  }
   const int d_raw = dblk * kBwdCh + cl;
   const bool active = d_raw < Dn;
   const int d = active ? d_raw : Dn - 1;
-  const int n0 = hf * NH;  // first state of this thread
   const int32_t* pos_row = a.pos + (int64_t)r * L;
   float* wsp = a.ws_param + (int64_t)(r * a.nseg + k) * (N + 2) * Dn;
-
-  int s0, s1;
-  segment_bounds(pos_row, L, k, a.nseg, sm.s_red, s0, s1);
   if (s0 >= s1) {
     if (active) {
 #pragma unroll
@@ -343,16 +454,8 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         wsp[(int64_t)(N + 1) * Dn + d] = 0.f;
       }
     }
-    return;
+    continue;
   }
-  // sub-chunk start states live in tensor memory (one TMEM lane per thread,
-  // kBNSub * NH fp32 columns), freeing shared memory for a 4th CTA per SM.
-  constexpr uint32_t kTmemCols = (kBNSub * NH <= 32) ? 32u : (kBNSub * NH <= 64 ? 64u : 128u);
-  if (wid == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tbase = sm.tmem_base + ((uint32_t)((wid & 3) * 32) << 16);
 
   const T* B_r = static_cast<const T*>(a.B) + (int64_t)r * N * L;
   const T* C_r = static_cast<const T*>(a.C) + (int64_t)r * N * L;
@@ -644,6 +747,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
       wsp[(int64_t)(N + 1) * Dn + d] = ddtb;
     }
   }
+  }  // work loop
   tmem_fence_before();
   __syncthreads();
   if (wid == 0) {
@@ -706,18 +810,33 @@ int n_chunks(int64_t L) { return (int)((L + kChunk - 1) / kChunk); }
 int n_dblk(int64_t Dn) { return (int)((Dn + kScanThreads - 1) / kScanThreads); }
 int n_dblk_bwd(int64_t Dn) { return (int)((Dn + kBwdCh - 1) / kBwdCh); }
 
-// Segments per row: enough CTAs for ~4 waves of the kernel's resident CTAs
-// on 148 SMs, but keep nominal segments >= 256 steps (cuts snap to heads).
-int n_segments(int64_t R, int64_t nblk, int64_t L, int64_t resident_per_sm) {
-  const int64_t ctas = R * nblk;
-  const int64_t target = 4 * 148 * resident_per_sm;
-  int64_t s = (target + ctas - 1) / ctas;
-  s = std::min<int64_t>(s, std::max<int64_t>(1, L / 256));
-  s = std::max<int64_t>(s, 1);
-  return (int)std::min<int64_t>(s, 64);
+// Segments per row: nominal cut every 256 steps (cuts snap to heads, so with
+// the paper's length distribution a segment is ~one sequence), <= 64.
+int n_seg(int64_t L) { return (int)std::max<int64_t>(1, std::min<int64_t>(64, L / 256)); }
+
+// states buffer = fp32 chunk states | 256 B counters | sorted segment list |
+// unsorted segment list (the fwd writes the schedule; the bwd reuses it)
+size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+size_t states_f32_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  return (size_t)R * n_chunks(L) * N * Dn * sizeof(float);
 }
-int nseg_fwd(int64_t R, int64_t Dn, int64_t L) { return n_segments(R, n_dblk(Dn), L, 4); }
-int nseg_bwd(int64_t R, int64_t Dn, int64_t L) { return n_segments(R, n_dblk_bwd(Dn), L, 3); }
+size_t sched_bytes(int64_t R, int64_t L) { return 256 + 2 * up256((size_t)R * n_seg(L) * 16); }
+size_t state_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  return up256(states_f32_bytes(R, Dn, L, N)) + sched_bytes(R, L);
+}
+struct Sched {
+  int* counters;
+  int4* sorted;
+  int4* unsorted;
+};
+Sched sched_of(void* states, int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  char* b = static_cast<char*>(states) + up256(states_f32_bytes(R, Dn, L, N));
+  Sched sc;
+  sc.counters = reinterpret_cast<int*>(b);
+  sc.sorted = reinterpret_cast<int4*>(b + 256);
+  sc.unsorted = reinterpret_cast<int4*>(b + 256 + up256((size_t)R * n_seg(L) * 16));
+  return sc;
+}
 
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -726,7 +845,7 @@ pm_status check_common(int64_t R, int64_t Dn, int64_t L, int32_t N, pm_dtype io)
   if (io != PM_F32 && io != PM_BF16) return PM_ERR_DTYPE;
   if (N != 4 && N != 8 && N != 16) return PM_ERR_UNSUPPORTED;
   if (R * L >= (int64_t(1) << 31) || Dn >= (int64_t(1) << 31)) return PM_ERR_SHAPE;
-  if (R > 65535) return PM_ERR_SHAPE;
+  if (R > 65535 || R * n_seg(L) * ((Dn + kBwdCh - 1) / kBwdCh) >= (int64_t(1) << 31)) return PM_ERR_SHAPE;
   return PM_OK;
 }
 
@@ -743,14 +862,46 @@ int tune_env(const char* name, int dflt) {
   return v ? atoi(v) : dflt;
 }
 
+// persistent grid: resident CTAs on all SMs, capped by the number of items
+template <typename K>
+int persistent_grid(K kern, int threads, size_t smem, int64_t items) {
+  int dev = 0, nsm = 148, nb = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
+  const int64_t g = (int64_t)nsm * std::max(nb, 1);
+  if (getenv("PM_DEBUG"))
+    fprintf(stderr, "[pm] persistent grid: nsm=%d blocks/SM=%d (err=%d) smem=%zu items=%lld -> %lld\n",
+            nsm, nb, (int)e, smem, (long long)items, (long long)std::min<int64_t>(g, items));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, items));
+}
+
+template <typename T, int N, bool kVec, int MinB>
+void fwd_go(const ScanFwdArgs& a, cudaStream_t s) {
+  auto kern = scan_fwd_kernel<T, N, kVec, MinB>;
+  if (a.items != nullptr) {
+    const int g = persistent_grid(kern, kScanThreads, 0, (int64_t)a.n_items * n_dblk(a.Dn));
+    kern<<<g, kScanThreads, 0, s>>>(a);
+  } else {
+    kern<<<dim3(n_dblk(a.Dn), a.R, a.nseg), kScanThreads, 0, s>>>(a);
+  }
+}
+
 template <typename T, int N, bool kVec>
 pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
-  dim3 grid(n_dblk(a.Dn), a.R, a.nseg);
+  if (a.items != nullptr) {  // schedule: plan + sort (reads pos only), reset counter
+    Sched sc = sched_of(a.states, a.R, a.Dn, a.L, N);
+    if (cudaMemsetAsync(sc.counters, 0, 256, s) != cudaSuccess) return PM_ERR_CUDA;
+    seg_plan_kernel<<<a.R, 256, 0, s>>>(a.pos, a.L, a.nseg, sc.unsorted);
+    PM_LAUNCH_CHECK();
+    seg_sort_kernel<<<1, 1024, 0, s>>>(sc.unsorted, a.n_items, sc.sorted);
+    PM_LAUNCH_CHECK();
+  }
   switch (tune_env("PM_TUNE_FWD_MINB", kFwdMinB)) {
-    case 3: scan_fwd_kernel<T, N, kVec, 3><<<grid, kScanThreads, 0, s>>>(a); break;
-    case 5: scan_fwd_kernel<T, N, kVec, 5><<<grid, kScanThreads, 0, s>>>(a); break;
-    case 6: scan_fwd_kernel<T, N, kVec, 6><<<grid, kScanThreads, 0, s>>>(a); break;
-    default: scan_fwd_kernel<T, N, kVec, 4><<<grid, kScanThreads, 0, s>>>(a); break;
+    case 3: fwd_go<T, N, kVec, 3>(a, s); break;
+    case 5: fwd_go<T, N, kVec, 5>(a, s); break;
+    case 6: fwd_go<T, N, kVec, 6>(a, s); break;
+    default: fwd_go<T, N, kVec, 4>(a, s); break;
   }
   PM_LAUNCH_CHECK();
   return PM_OK;
@@ -778,8 +929,28 @@ pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, floa
                                                           : scan_bwd_kernel<T, N, kVec, 4>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return PM_ERR_CUDA;
-  dim3 grid(n_dblk_bwd(a.Dn), a.R, a.nseg);
-  kern<<<grid, kBwdThreads, smem, s>>>(a);
+  // prefer the maximum shared-memory carveout so 4 CTAs (54 KB each) fit per SM
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+    return PM_ERR_CUDA;
+  if (a.items != nullptr) {
+    if (cudaMemsetAsync(a.counter, 0, sizeof(int), s) != cudaSuccess) return PM_ERR_CUDA;
+    // resident CTAs per SM: register cap (launch bounds) and 228 KB of shared
+    // memory per SM (1 KB reserved per CTA); the occupancy API under-reports
+    // this kernel, so the grid is sized from the limits directly.
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int minb = tune_env("PM_TUNE_BWD_MINB", kBwdMinB) == 3 ? 3 : 4;
+    const int nb = std::max(1, std::min<int>(minb, (int)((228 * 1024) / (smem + 1024))));
+    const int64_t items = (int64_t)a.n_items * n_dblk_bwd(a.Dn);
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * nb, items));
+    if (getenv("PM_DEBUG"))
+      fprintf(stderr, "[pm] bwd persistent grid: %d x %d CTAs/SM (smem %zu) -> %d\n", nsm, nb, smem, g);
+    kern<<<g, kBwdThreads, smem, s>>>(a);
+  } else {
+    kern<<<dim3(n_dblk_bwd(a.Dn), a.R, a.nseg), kBwdThreads, smem, s>>>(a);
+  }
   PM_LAUNCH_CHECK();
   dim3 g2((a.L + 31) / 32, a.R);
   scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
@@ -808,16 +979,16 @@ pm_status dispatch_bwd(const ScanBwdArgs& a, int N, bool vec, float* dA, float* 
   }
 }
 
-size_t state_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
-  return (size_t)R * n_chunks(L) * N * Dn * sizeof(float);
+// bwd workspace = dB/dC partials | param partials | counter | (recomputed states)
+size_t ws_bc_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  return up256((size_t)n_dblk_bwd(Dn) * R * L * 2 * N * sizeof(float));
 }
-
+size_t ws_par_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  return up256((size_t)R * n_seg(L) * (N + 2) * Dn * sizeof(float));
+}
 size_t bwd_ws_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N, bool recompute) {
-  size_t bc = (size_t)n_dblk_bwd(Dn) * R * L * 2 * N * sizeof(float);
-  size_t par = (size_t)R * nseg_bwd(R, Dn, L) * (N + 2) * Dn * sizeof(float);
-  size_t st = recompute ? state_bytes(R, Dn, L, N) : 0;
-  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
-  return up(bc) + up(par) + up(st);
+  return ws_bc_bytes(R, Dn, L, N) + ws_par_bytes(R, Dn, L, N) + 256 +
+         (recompute ? up256(state_bytes(R, Dn, L, N)) : 0);
 }
 
 }  // namespace
@@ -845,14 +1016,20 @@ pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, c
   if (!u || !dt || !A || !B || !C || !pos || (!y && !states)) return PM_ERR_INVALID_ARG;
   for (const void* p : {u, dt, B, C, (const void*)y})
     if (!elem_aligned(p, io)) return PM_ERR_ALIGN;
-  for (const void* p : {(const void*)A, (const void*)Dskip, (const void*)dt_bias, (const void*)pos,
-                        (const void*)states})
+  for (const void* p : {(const void*)A, (const void*)Dskip, (const void*)dt_bias, (const void*)pos})
     if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
+  if (!aligned16(states)) return PM_ERR_ALIGN;
   const int isz = io == PM_F32 ? 4 : 2;
   const bool vec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
                    aligned16(C) && aligned16(y);
-  ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, y, states,
-                (int)R, (int)Dn, (int)L, nseg_fwd(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
+  ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, y, states, nullptr, nullptr, 0,
+                (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0};
+  if (states != nullptr) {  // persistent longest-first schedule lives in the states buffer
+    Sched sc = sched_of(states, R, Dn, L, N);
+    a.items = sc.sorted;
+    a.counter = sc.counters;
+    a.n_items = (int)(R * n_seg(L));
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return io == PM_F32 ? dispatch_fwd<float>(a, N, vec, s) : dispatch_fwd<__nv_bfloat16>(a, N, vec, s);
 }
@@ -870,36 +1047,46 @@ pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, c
     return PM_ERR_INVALID_ARG;
   const bool recompute = states == nullptr;
   if (!workspace || ws_bytes < bwd_ws_bytes(R, Dn, L, N, recompute)) return PM_ERR_WORKSPACE;
-  if (!aligned16(workspace)) return PM_ERR_ALIGN;
+  if (!aligned16(workspace) || !aligned16(states)) return PM_ERR_ALIGN;
   for (const void* p : {u, dt, B, C, dy, (const void*)du, (const void*)ddt})
     if (!elem_aligned(p, io)) return PM_ERR_ALIGN;
   for (const void* p : {(const void*)A, (const void*)Dskip, (const void*)dt_bias, (const void*)pos,
-                        (const void*)states, (const void*)dA, (const void*)dB, (const void*)dC,
-                        (const void*)dD, (const void*)ddt_bias})
+                        (const void*)dA, (const void*)dB, (const void*)dC, (const void*)dD,
+                        (const void*)ddt_bias})
     if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
   const int isz = io == PM_F32 ? 4 : 2;
   const bool vec = (L * isz) % 16 == 0 && Dn % 4 == 0 && aligned16(u) && aligned16(dt) &&
                    aligned16(B) && aligned16(C) && aligned16(dy) && aligned16(du) &&
-                   aligned16(ddt) && aligned16(states);
+                   aligned16(ddt);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
   char* w = static_cast<char*>(workspace);
   float* ws_bc = reinterpret_cast<float*>(w);
-  w += up((size_t)n_dblk_bwd(Dn) * R * L * 2 * N * sizeof(float));
+  w += ws_bc_bytes(R, Dn, L, N);
   float* ws_par = reinterpret_cast<float*>(w);
-  w += up((size_t)R * nseg_bwd(R, Dn, L) * (N + 2) * Dn * sizeof(float));
+  w += ws_par_bytes(R, Dn, L, N);
+  int* counter = reinterpret_cast<int*>(w);
+  w += 256;
   const float* stp = states;
   if (recompute) {
     float* st_ws = reinterpret_cast<float*>(w);
-    ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws,
-                   (int)R, (int)Dn, (int)L, nseg_fwd(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
-    pm_status fs = io == PM_F32 ? dispatch_fwd<float>(fa, N, vec, s)
-                                : dispatch_fwd<__nv_bfloat16>(fa, N, vec, s);
+    ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws, nullptr, nullptr, 0,
+                   (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0};
+    Sched sc = sched_of(st_ws, R, Dn, L, N);
+    fa.items = sc.sorted;
+    fa.counter = sc.counters;
+    fa.n_items = (int)(R * n_seg(L));
+    const bool fvec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
+                      aligned16(C);
+    pm_status fs = io == PM_F32 ? dispatch_fwd<float>(fa, N, fvec, s)
+                                : dispatch_fwd<__nv_bfloat16>(fa, N, fvec, s);
     if (fs != PM_OK) return fs;
     stp = st_ws;
   }
+  // the length-sorted segment list written by the forward pass
+  const Sched sc = sched_of(const_cast<float*>(stp), R, Dn, L, N);
   ScanBwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, stp, dy, du, ddt, ws_bc, ws_par,
-                (int)R, (int)Dn, (int)L, nseg_bwd(R, Dn, L), n_chunks(L), dt_softplus ? 1 : 0};
+                sc.sorted, counter, (int)(R * n_seg(L)),
+                (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0};
   return io == PM_F32 ? dispatch_bwd<float>(a, N, vec, dA, dB, dC, dD, ddt_bias, s)
                       : dispatch_bwd<__nv_bfloat16>(a, N, vec, dA, dB, dC, dD, ddt_bias, s);
 }

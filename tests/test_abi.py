@@ -88,8 +88,10 @@ def test_validation_before_launch():
     # bf16: odd address is misaligned, even is fine for validation
     assert L.pm_selective_scan_fwd(_vp(0x1001), *([p] * 6), 1, p, p, p, 2, 8, 64, 16, 1,
                                    None) == 5
-    # state bytes: (R, ceil(L/16), N, Dn) fp32
-    assert L.pm_selective_scan_state_bytes(2, 8, 64, 16) == 2 * 4 * 16 * 8 * 4
+    # state bytes: (R, ceil(L/16), N, Dn) fp32 states (256-B aligned) + the
+    # segment schedule (256 B counters + 2 lists of R*nseg int4, 256-B aligned)
+    up = lambda x: (x + 255) // 256 * 256
+    assert L.pm_selective_scan_state_bytes(2, 8, 64, 16) == up(2 * 4 * 16 * 8 * 4) + 256 + 2 * up(2 * 1 * 16)
 
 
 def test_pack_query_mode_and_capacity():
