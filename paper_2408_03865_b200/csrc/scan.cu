@@ -111,19 +111,48 @@ __global__ void __launch_bounds__(256) seg_plan_kernel(const int32_t* __restrict
     items[r * nseg + k] = make_int4(r, k, cut[k], max(cut[k], cut[k + 1]));
 }
 
-// rank sort by length (descending), ties by index: O(n^2 / threads)
-__global__ void __launch_bounds__(1024) seg_sort_kernel(const int4* __restrict__ in, int n,
+// Longest-first order of the segment list (one CTA).  n <= 4096: exact rank
+// sort (length descending, ties by index); larger n: bucket sort on 1024
+// length bins (order within a bin is arbitrary -- results never depend on
+// the processing order, only the load balance does).
+__global__ void __launch_bounds__(1024) seg_sort_kernel(const int4* __restrict__ in, int n, int L,
                                                        int4* __restrict__ out) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int4 a = in[i];
-    const int la = a.w - a.z;
-    int rank = 0;
-    for (int j = 0; j < n; ++j) {
-      const int4 b = in[j];
-      const int lb = b.w - b.z;
-      rank += (lb > la) || (lb == la && j < i);
+  if (n <= 4096) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int4 a = in[i];
+      const int la = a.w - a.z;
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const int4 b = in[j];
+        const int lb = b.w - b.z;
+        rank += (lb > la) || (lb == la && j < i);
+      }
+      out[rank] = a;
     }
-    out[rank] = a;
+    return;
+  }
+  constexpr int kBins = 1024;
+  __shared__ int cnt[kBins];
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  auto bin_of = [&](const int4 v) {  // longest first: bin 0 = longest
+    const int len = v.w - v.z;
+    return kBins - 1 - (int)(((int64_t)len * (kBins - 1)) / max(L, 1));
+  };
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[bin_of(in[i])], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan -> bin cursors
+    int acc = 0;
+    for (int b = 0; b < kBins; ++b) {
+      const int c = cnt[b];
+      cnt[b] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int4 v = in[i];
+    out[atomicAdd(&cnt[bin_of(v)], 1)] = v;
   }
 }
 
@@ -894,7 +923,7 @@ pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
     if (cudaMemsetAsync(sc.counters, 0, 256, s) != cudaSuccess) return PM_ERR_CUDA;
     seg_plan_kernel<<<a.R, 256, 0, s>>>(a.pos, a.L, a.nseg, sc.unsorted);
     PM_LAUNCH_CHECK();
-    seg_sort_kernel<<<1, 1024, 0, s>>>(sc.unsorted, a.n_items, sc.sorted);
+    seg_sort_kernel<<<1, 1024, 0, s>>>(sc.unsorted, a.n_items, a.L, sc.sorted);
     PM_LAUNCH_CHECK();
   }
   switch (tune_env("PM_TUNE_FWD_MINB", kFwdMinB)) {
