@@ -75,6 +75,10 @@ def lib():
                                                      _i64, _i64, _i32]
         L.pmo_seq_scan_bwd.argtypes = ([_f64p] * 7 + [_i32] + [_f64p] * 8 +
                                        [_i64, _i64, _i32])
+        L.pmo_scan_fwd_ext.argtypes = ([_f64p] * 7 + [_i32, _i32p, _f64p, _f64p, _f64p, _f64p,
+                                        _i64, _i64, _i64, _i32])
+        L.pmo_scan_bwd_ext.argtypes = ([_f64p] * 7 + [_i32, _i32p] + [_f64p] * 13 +
+                                       [_i64, _i64, _i64, _i32])
         L.pmo_num_threads.restype = ctypes.c_int
         L.pmo_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -280,3 +284,42 @@ def seq_scan_bwd(u, dt, A, B, C, D, dt_bias, dy, acc, softplus=True):
                            _p(ddt), _p(acc["dA"]), _p(dB), _p(dC),
                            _p(acc["dD"]), _p(acc["ddt_bias"]), Dn, Ls, N)
     return du, ddt, dB, dC
+
+
+# --- NEXT-1 / NEXT-2: gate and state passing ---------------------------------
+
+def scan_fwd_ext(u, dt, A, B, C, D, dt_bias, pos, z=None, h0=None, softplus=True):
+    """Returns (out, h_last): out = y * silu(z) (y if z is None); h0 (R,Dn,N)
+    is the state entering t=0 when pos[r,0] != 0."""
+    u, dt, A, B, C = _f64(u), _f64(dt), _f64(A), _f64(B), _f64(C)
+    D, dt_bias, z, h0 = _f64(D), _f64(dt_bias), _f64(z), _f64(h0)
+    pos = np.ascontiguousarray(pos, dtype=np.int32)
+    R, Dn, L = u.shape
+    N = A.shape[1]
+    out = np.empty_like(u)
+    h_last = np.empty((R, Dn, N))
+    lib().pmo_scan_fwd_ext(_p(u), _p(dt), _p(A), _p(B), _p(C), _p(D), _p(dt_bias),
+                           int(bool(softplus)), _p(pos, _i32p), _p(z), _p(h0), _p(out),
+                           _p(h_last), R, Dn, L, N)
+    return out, h_last
+
+
+def scan_bwd_ext(u, dt, A, B, C, D, dt_bias, pos, dout, z=None, h0=None, dh_last=None,
+                 softplus=True):
+    """Adjoint of scan_fwd_ext -> dict(du, ddt, dA, dB, dC, dD, ddt_bias, dz, dh0)."""
+    u, dt, A, B, C = _f64(u), _f64(dt), _f64(A), _f64(B), _f64(C)
+    D, dt_bias, z, h0 = _f64(D), _f64(dt_bias), _f64(z), _f64(h0)
+    dout, dh_last = _f64(dout), _f64(dh_last)
+    pos = np.ascontiguousarray(pos, dtype=np.int32)
+    R, Dn, L = u.shape
+    N = A.shape[1]
+    o = dict(du=np.zeros_like(u), ddt=np.zeros_like(u), dA=np.empty((Dn, N)),
+             dB=np.zeros((R, N, L)), dC=np.zeros((R, N, L)), dD=np.empty(Dn),
+             ddt_bias=np.empty(Dn), dz=np.zeros_like(u) if z is not None else None,
+             dh0=np.zeros((R, Dn, N)) if h0 is not None else None)
+    lib().pmo_scan_bwd_ext(_p(u), _p(dt), _p(A), _p(B), _p(C), _p(D), _p(dt_bias),
+                           int(bool(softplus)), _p(pos, _i32p), _p(z), _p(h0), _p(dout),
+                           _p(dh_last), _p(o["du"]), _p(o["ddt"]), _p(o["dA"]), _p(o["dB"]),
+                           _p(o["dC"]), _p(o["dD"]), _p(o["ddt_bias"]), _p(o["dz"]),
+                           _p(o["dh0"]), R, Dn, L, N)
+    return o

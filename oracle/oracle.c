@@ -536,3 +536,158 @@ void pmo_seq_scan_bwd(const double* u, const double* dt, const double* A,
     free(hs);
     free(g);
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-1 / NEXT-2: the full selective-scan signature.        */
+/*   z (R,Dn,L) or NULL : gate, out = y * silu(z) (the paper's element-wise   */
+/*                        sigmoid op; Fig 1)                          */
+/*   h0 (R,Dn,N) or NULL: state entering t = 0 of each row when that slot is  */
+/*                        NOT a sequence start (pos[r,0] != 0) -- the state   */
+/*                        passing between cut parts of a long sequence that   */
+/*                        the paper plans as future work             */
+/*   h_last (R,Dn,N) or NULL: state after step L-1 of each row               */
+/* head(r,t) := pos[r,t] == 0 || (t == 0 && h0 == NULL).                     */
+/* ------------------------------------------------------------------------ */
+
+static int is_head_ext(const int32_t* pos_row, int64_t t, const double* h0) {
+    return pos_row[t] == 0 || (t == 0 && h0 == NULL);
+}
+
+void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
+                      const double* B, const double* C, const double* D,
+                      const double* dt_bias, int32_t softplus,
+                      const int32_t* pos, const double* z, const double* h0,
+                      double* out, double* h_last,
+                      int64_t R, int64_t Dn, int64_t L, int32_t N) {
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int64_t r = 0; r < R; ++r)
+        for (int64_t d = 0; d < Dn; ++d) {
+            double* h = (double*)calloc((size_t)N, sizeof(double));
+            const int64_t lane = (r * Dn + d) * L;
+            if (h0)
+                for (int32_t n = 0; n < N; ++n) h[n] = h0[(r * Dn + d) * N + n];
+            for (int64_t t = 0; t < L; ++t) {
+                double v = dt[lane + t] + (dt_bias ? dt_bias[d] : 0.0);
+                double delta = softplus ? softplus_d(v) : v;
+                double x = u[lane + t];
+                double yt = 0.0;
+                const int head = is_head_ext(pos + r * L, t, h0);
+                for (int32_t n = 0; n < N; ++n) {
+                    double bx = delta * B[(r * N + n) * L + t] * x;
+                    h[n] = head ? bx : exp(delta * A[d * N + n]) * h[n] + bx;
+                    yt += C[(r * N + n) * L + t] * h[n];
+                }
+                yt += (D ? D[d] : 0.0) * x;
+                if (z) {
+                    double zz = z[lane + t];
+                    yt = yt * zz * sigmoid_d(zz);
+                }
+                out[lane + t] = yt;
+            }
+            if (h_last)
+                for (int32_t n = 0; n < N; ++n) h_last[(r * Dn + d) * N + n] = h[n];
+            free(h);
+        }
+}
+
+/* Adjoint of pmo_scan_fwd_ext.  dout is the cotangent of `out`; dh_last
+ * (or NULL) the cotangent of h_last.  Extra outputs: dz (if z), dh0 (if h0).
+ * Param grads (dA, dD, ddt_bias) and dB, dC are overwritten sums. */
+void pmo_scan_bwd_ext(const double* u, const double* dt, const double* A,
+                      const double* B, const double* C, const double* D,
+                      const double* dt_bias, int32_t softplus,
+                      const int32_t* pos, const double* z, const double* h0,
+                      const double* dout, const double* dh_last,
+                      double* du, double* ddt, double* dA, double* dB,
+                      double* dC, double* dD, double* ddt_bias, double* dz,
+                      double* dh0, int64_t R, int64_t Dn, int64_t L, int32_t N) {
+    const int nth = pmo_num_threads();
+    const size_t bc = (size_t)R * (size_t)N * (size_t)L;
+    double* pB = (double*)calloc((size_t)nth * bc, sizeof(double));
+    double* pC = (double*)calloc((size_t)nth * bc, sizeof(double));
+    for (int64_t i = 0; i < Dn * N; ++i) dA[i] = 0.0;
+    for (int64_t d = 0; d < Dn; ++d) {
+        if (dD) dD[d] = 0.0;
+        if (ddt_bias) ddt_bias[d] = 0.0;
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t d = 0; d < Dn; ++d) {
+#ifdef _OPENMP
+        const int tid = omp_get_thread_num();
+#else
+        const int tid = 0;
+#endif
+        double* hs = (double*)malloc(sizeof(double) * (size_t)((L + 1) * N));
+        double* as = (double*)malloc(sizeof(double) * (size_t)(L * N));
+        double* g = (double*)malloc(sizeof(double) * (size_t)N);
+        double* carry = (double*)malloc(sizeof(double) * (size_t)N);
+        for (int64_t r = 0; r < R; ++r) {
+            const int64_t lane = (r * Dn + d) * L;
+            const int32_t* pr = pos + r * L;
+            double* myB = pB + (size_t)tid * bc + (size_t)r * N * L;
+            double* myC = pC + (size_t)tid * bc + (size_t)r * N * L;
+            /* forward: hs[(t+1)N + n] = h_t, hs[n] = h_{-1} (h0 or 0) */
+            for (int32_t n = 0; n < N; ++n) hs[n] = h0 ? h0[(r * Dn + d) * N + n] : 0.0;
+            for (int64_t t = 0; t < L; ++t) {
+                double v = dt[lane + t] + (dt_bias ? dt_bias[d] : 0.0);
+                double delta = softplus ? softplus_d(v) : v;
+                const int head = is_head_ext(pr, t, h0);
+                for (int32_t n = 0; n < N; ++n) {
+                    double abar = head ? 0.0 : exp(delta * A[d * N + n]);
+                    double bx = delta * B[(r * N + n) * L + t] * u[lane + t];
+                    hs[(t + 1) * N + n] = head ? bx : abar * hs[t * N + n] + bx;
+                    as[t * N + n] = abar;
+                }
+            }
+            for (int32_t n = 0; n < N; ++n) carry[n] = dh_last ? dh_last[(r * Dn + d) * N + n] : 0.0;
+            for (int64_t t = L - 1; t >= 0; --t) {
+                double v = dt[lane + t] + (dt_bias ? dt_bias[d] : 0.0);
+                double delta = softplus ? softplus_d(v) : v;
+                double x = u[lane + t];
+                /* y_t (pre-gate) and the gate's chain rule */
+                double yt = (D ? D[d] : 0.0) * x;
+                for (int32_t n = 0; n < N; ++n)
+                    yt += C[(r * N + n) * L + t] * hs[(t + 1) * N + n];
+                double gy = dout[lane + t];
+                if (z) {
+                    double zz = z[lane + t], s = sigmoid_d(zz);
+                    dz[lane + t] = gy * yt * s * (1.0 + zz * (1.0 - s));
+                    gy = gy * zz * s;
+                }
+                double S = 0.0, dq = 0.0;
+                for (int32_t n = 0; n < N; ++n) {
+                    g[n] = C[(r * N + n) * L + t] * gy + carry[n];
+                    S += g[n] * B[(r * N + n) * L + t];
+                    double q = g[n] * as[t * N + n] * hs[t * N + n];
+                    dq += A[d * N + n] * q;
+                    dA[d * N + n] += delta * q;
+                    myB[n * L + t] += g[n] * delta * x;
+                    myC[n * L + t] += gy * hs[(t + 1) * N + n];
+                    carry[n] = as[t * N + n] * g[n];
+                }
+                du[lane + t] = (D ? D[d] : 0.0) * gy + delta * S;
+                double gd = (x * S + dq) * (softplus ? sigmoid_d(v) : 1.0);
+                ddt[lane + t] = gd;
+                if (dD) dD[d] += gy * x;
+                if (ddt_bias) ddt_bias[d] += gd;
+            }
+            /* carry now holds abar_0 * g_0 = dL/dh_{-1} (0 when t = 0 is a head) */
+            if (dh0)
+                for (int32_t n = 0; n < N; ++n) dh0[(r * Dn + d) * N + n] = carry[n];
+        }
+        free(hs); free(as); free(g); free(carry);
+    }
+    for (int64_t r = 0; r < R; ++r)
+        for (int32_t n = 0; n < N; ++n)
+            for (int64_t t = 0; t < L; ++t) {
+                double sb = 0.0, sc = 0.0;
+                for (int k = 0; k < nth; ++k) {
+                    sb += pB[(size_t)k * bc + ((size_t)r * N + n) * L + t];
+                    sc += pC[(size_t)k * bc + ((size_t)r * N + n) * L + t];
+                }
+                dB[(r * N + n) * L + t] = sb;
+                dC[(r * N + n) * L + t] = sc;
+            }
+    free(pB);
+    free(pC);
+}
