@@ -96,6 +96,9 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        t0 = time.time()  # wait for the sampler to be live before the timed region
+        while not self.samples and time.time() - t0 < 5.0:
+            time.sleep(0.01)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -120,7 +123,7 @@ class ClockSampler:
                 continue
             rows.append((ts, parts))
         inside = [p for ts, p in rows if self.t_on and self.t_on - 0.06 <= ts <= self.t_off + 0.06]
-        use = inside if inside else rows
+        use = inside if inside else [p for _, p in rows]
         if not use:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
 

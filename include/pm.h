@@ -217,6 +217,58 @@ PM_API pm_status pm_selective_scan_bwd(const void* u, const void* dt,
                                 int64_t L, int32_t N, pm_dtype io,
                                 pm_stream_t stream);
 
+/* ===========================================================================
+ * Extended scan: the fused gate and cross-row state passing
+ *   (the element-wise sigmoid/silu gate of the Mamba
+ *    block, P:135 and Fig 1; NEXT-2: "cut long sequences and pass the hidden
+ *    state between the parts", the paper's future work)
+ * ===========================================================================
+ * Same recurrence as pm_selective_scan_fwd, with:
+ *   z (optional, (R,Dn,L) io dtype):  out[r,d,t] = y[r,d,t] * silu(z[r,d,t]),
+ *     silu(z) = z / (1 + exp(-z)); with z == NULL, out = y.
+ *   h0 (optional, (R,Dn,N) fp32): the state entering slot 0 of each row.
+ *     With h0 != NULL slot 0 is a head only when pos[r,0] == 0; otherwise it
+ *     continues h0[r] (abar_0 = exp(delta_0 A)).  With h0 == NULL slot 0 is
+ *     always a head (the base ABI).
+ *   h_last (optional, (R,Dn,N) fp32): written with the state after slot L-1
+ *     (the input of the next part of a cut sequence).
+ * At least one of out, states, h_last must be non-NULL.  Pointers are device
+ * memory owned by the caller; h0/h_last must not alias. */
+PM_API pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt,
+                                   const float* A, const void* B,
+                                   const void* C, const float* Dskip,
+                                   const float* dt_bias, int32_t dt_softplus,
+                                   const int32_t* pos, const void* z,
+                                   const float* h0, void* out, float* states,
+                                   float* h_last, int64_t R, int64_t Dn,
+                                   int64_t L, int32_t N, pm_dtype io,
+                                   pm_stream_t stream);
+
+/* Backward of pm_selective_scan_fwd_ex, given dout = dLoss/d(out) and
+ * dh_last = dLoss/d(h_last) (optional, (R,Dn,N) fp32; NULL = 0):
+ *   dy  = dout * silu(z)                (dy = dout when z == NULL)
+ *   dz  = dout * y * silu'(z),  silu'(z) = s (1 + z (1 - s)), s = sigmoid(z)
+ *   the carry into slot L-1 starts at dh_last instead of 0;
+ *   dh0 (optional, (R,Dn,N) fp32) = dLoss/dh0 = abar_0 g_0 (0 when slot 0 is
+ *     a head);
+ * the other outputs as pm_selective_scan_bwd.  dz is required iff z != NULL
+ * (io dtype, (R,Dn,L)).  states: the buffer filled by the forward pass on
+ * the SAME inputs (incl. h0), or NULL to recompute.  Workspace as
+ * pm_selective_scan_bwd_workspace(). */
+PM_API pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt,
+                                   const float* A, const void* B,
+                                   const void* C, const float* Dskip,
+                                   const float* dt_bias, int32_t dt_softplus,
+                                   const int32_t* pos, const void* z,
+                                   const float* h0, const float* states,
+                                   const void* dout, const float* dh_last,
+                                   void* du, void* ddt, float* dA, float* dB,
+                                   float* dC, float* dD, float* ddt_bias,
+                                   void* dz, float* dh0, void* workspace,
+                                   size_t ws_bytes, int64_t R, int64_t Dn,
+                                   int64_t L, int32_t N, pm_dtype io,
+                                   pm_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

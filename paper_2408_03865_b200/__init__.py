@@ -18,7 +18,8 @@ __all__ = [
     "pm_pack", "pm_pack_planned", "pm_causal_conv1d_fwd", "pm_causal_conv1d_bwd",
     "pm_causal_conv1d_bwd_workspace", "pm_selective_scan_state_bytes",
     "pm_selective_scan_fwd", "pm_selective_scan_bwd",
-    "pm_selective_scan_bwd_workspace", "EXPORTED_SYMBOLS",
+    "pm_selective_scan_bwd_workspace", "pm_selective_scan_fwd_ex", "pm_selective_scan_bwd_ex",
+    "EXPORTED_SYMBOLS",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -34,7 +35,8 @@ EXPORTED_SYMBOLS = [
     "pm_status_string", "pm_version", "pm_plan_fifo", "pm_plan_greedy", "pm_pack",
     "pm_pack_planned", "pm_causal_conv1d_fwd", "pm_causal_conv1d_bwd_workspace",
     "pm_causal_conv1d_bwd", "pm_selective_scan_state_bytes", "pm_selective_scan_fwd",
-    "pm_selective_scan_bwd_workspace", "pm_selective_scan_bwd",
+    "pm_selective_scan_bwd_workspace", "pm_selective_scan_bwd", "pm_selective_scan_fwd_ex",
+    "pm_selective_scan_bwd_ex",
 ]
 
 
@@ -78,6 +80,10 @@ def lib():
         L.pm_selective_scan_bwd_workspace.argtypes = [_i64, _i64, _i64, _i32, _i32]
         L.pm_selective_scan_bwd.argtypes = ([_vp] * 7 + [_i32] + [_vp] * 10 + [_vp, _sz] +
                                             [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
+        L.pm_selective_scan_fwd_ex.argtypes = ([_vp] * 7 + [_i32] + [_vp] * 6 +
+                                               [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
+        L.pm_selective_scan_bwd_ex.argtypes = ([_vp] * 7 + [_i32] + [_vp] * 15 + [_vp, _sz] +
+                                               [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
         for f in EXPORTED_SYMBOLS:
             if f not in ("pm_status_string", "pm_version") and not f.endswith(
                     ("_workspace", "_bytes")):
@@ -302,4 +308,65 @@ def pm_selective_scan_bwd(u, dt, A, B, C, Dskip, dt_bias, pos, dy, states=None,
         _ptr(o["dA"]), _ptr(o["dB"]), _ptr(o["dC"]), _ptr(o["dD"]), _ptr(o["ddt_bias"]),
         _ptr(workspace), workspace.numel(), R, Dn, L, N, _io(u), _stream(u)),
         "pm_selective_scan_bwd")
+    return o
+
+
+def pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, z=None, h0=None, out=None,
+                             states=None, h_last=None, dt_softplus=True, want_states=True,
+                             want_last_state=False):
+    """Extended ScanOp_pack forward: fused gate ``out = y * silu(z)`` (SURVEY
+    NEXT-1) and cross-row state passing ``h0 -> h_last`` (NEXT-2, the
+    paper's future work P:275).  Returns (out, states, h_last)."""
+    import torch
+    _dev(u, dt, A, B, C, Dskip, dt_bias, pos, z, h0)
+    R, Dn, L = u.shape
+    N = A.shape[1]
+    out = torch.empty_like(u) if out is None else out
+    if states is None and want_states:
+        nb = pm_selective_scan_state_bytes(R, Dn, L, N)
+        states = torch.empty(nb // 4, dtype=torch.float32, device=u.device)
+    if h_last is None and want_last_state:
+        h_last = torch.empty((R, Dn, N), dtype=torch.float32, device=u.device)
+    _dev(out, states, h_last)
+    _check(lib().pm_selective_scan_fwd_ex(
+        _ptr(u), _ptr(dt), _ptr(A), _ptr(B), _ptr(C), _ptr(Dskip), _ptr(dt_bias),
+        int(bool(dt_softplus)), _ptr(pos), _ptr(z), _ptr(h0), _ptr(out), _ptr(states),
+        _ptr(h_last), R, Dn, L, N, _io(u), _stream(u)), "pm_selective_scan_fwd_ex")
+    return out, states, h_last
+
+
+def pm_selective_scan_bwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, dout, z=None, h0=None,
+                             states=None, dh_last=None, dt_softplus=True, out=None,
+                             workspace=None, want_dh0=None):
+    """Adjoint of pm_selective_scan_fwd_ex.  Returns dict du, ddt, dA, dB, dC,
+    dD, ddt_bias, dz (when z is given), dh0 (when h0 is given or want_dh0)."""
+    import torch
+    _dev(u, dt, A, B, C, Dskip, dt_bias, pos, dout, z, h0, states, dh_last)
+    R, Dn, L = u.shape
+    N = A.shape[1]
+    o = dict(out or {})
+    dev = u.device
+    f32 = dict(dtype=torch.float32, device=dev)
+    o.setdefault("du", torch.empty_like(u))
+    o.setdefault("ddt", torch.empty_like(u))
+    o.setdefault("dA", torch.empty((Dn, N), **f32))
+    o.setdefault("dB", torch.empty((R, N, L), **f32))
+    o.setdefault("dC", torch.empty((R, N, L), **f32))
+    o.setdefault("dD", torch.empty((Dn,), **f32) if Dskip is not None else None)
+    o.setdefault("ddt_bias", torch.empty((Dn,), **f32) if dt_bias is not None else None)
+    o.setdefault("dz", torch.empty_like(u) if z is not None else None)
+    if want_dh0 is None:
+        want_dh0 = h0 is not None
+    o.setdefault("dh0", torch.empty((R, Dn, N), **f32) if want_dh0 else None)
+    need = pm_selective_scan_bwd_workspace(R, Dn, L, N, states is None)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    _dev(workspace, *[v for v in o.values() if v is not None])
+    _check(lib().pm_selective_scan_bwd_ex(
+        _ptr(u), _ptr(dt), _ptr(A), _ptr(B), _ptr(C), _ptr(Dskip), _ptr(dt_bias),
+        int(bool(dt_softplus)), _ptr(pos), _ptr(z), _ptr(h0), _ptr(states), _ptr(dout),
+        _ptr(dh_last), _ptr(o["du"]), _ptr(o["ddt"]), _ptr(o["dA"]), _ptr(o["dB"]),
+        _ptr(o["dC"]), _ptr(o["dD"]), _ptr(o["ddt_bias"]), _ptr(o["dz"]), _ptr(o["dh0"]),
+        _ptr(workspace), workspace.numel(), R, Dn, L, N, _io(u), _stream(u)),
+        "pm_selective_scan_bwd_ex")
     return o

@@ -52,6 +52,9 @@ struct ScanFwdArgs {
   int* counter;       // work counter for the persistent loop
   int n_items;
   int R, Dn, L, nseg, nchunk, softplus;
+  const void* z;      // NEXT-1 gate (R,Dn,L) or NULL: y <- y * silu(z)
+  const float* h0;    // NEXT-2 state entering t=0 (R,Dn,N) or NULL
+  float* h_last;      // state after step L-1 (R,Dn,N) or NULL
 };
 
 struct ScanBwdArgs {
@@ -73,6 +76,11 @@ struct ScanBwdArgs {
   int* counter;
   int n_items;
   int R, Dn, L, nseg, nchunk, softplus;
+  const void* z;        // NEXT-1 gate (R,Dn,L) or NULL; dy is then d(out)
+  const float* h0;      // NEXT-2 state entering t=0 (R,Dn,N) or NULL
+  const float* dh_last; // cotangent of the state after step L-1 or NULL
+  void* dz;             // (R,Dn,L) when z != NULL
+  float* dh0;           // (R,Dn,N) when h0 != NULL
 };
 
 // ---------------------------------------------------------------------------
@@ -167,7 +175,7 @@ struct Work {
 template <typename T, int N, int W, bool kVec>
 PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
                      const int32_t* __restrict__ pos_row, int L, int j0,
-                     float (*sB)[N], float (*sC)[N], unsigned* sMask) {
+                     float (*sB)[N], float (*sC)[N], unsigned* sMask, bool t0_head) {
   static_assert(W % 8 == 0, "window must be a multiple of 8");
   for (int e = threadIdx.x; e < N * (W / 8); e += blockDim.x) {
     const int n = e % N, tb = (e / N) * 8;
@@ -185,7 +193,8 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
 #pragma unroll
     for (int w0 = 0; w0 < W; w0 += 32) {
       const int t = j0 + w0 + (int)threadIdx.x;
-      const bool f = (w0 + (int)threadIdx.x < W) && ((t >= L) || t == 0 || __ldg(pos_row + t) == 0);
+      const bool f = (w0 + (int)threadIdx.x < W) &&
+                     ((t >= L) || (t == 0 && t0_head) || __ldg(pos_row + t) == 0);
       const unsigned m = __ballot_sync(0xffffffffu, f);
       if (threadIdx.x == 0) sMask[w0 / 32] = m;
     }
@@ -195,7 +204,7 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
-template <typename T, int N, bool kVec, int MinB>
+template <typename T, int N, bool kVec, int MinB, bool kGate>
 __global__ void __launch_bounds__(kScanThreads, MinB)
 scan_fwd_kernel(const ScanFwdArgs a) {
   __shared__ __align__(16) float sB[kTile][N];
@@ -237,6 +246,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   const T* u_row = static_cast<const T*>(a.u) + lane;
   const T* dt_row = static_cast<const T*>(a.dt) + lane;
   T* y_row = a.y ? static_cast<T*>(a.y) + lane : nullptr;
+  const T* z_row = kGate ? static_cast<const T*>(a.z) + lane : nullptr;
 
   // states are processed in pairs with packed fp32x2 arithmetic (FFMA2)
   constexpr int NP = N / 2;
@@ -251,33 +261,41 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   float2 h[NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
+  if (s0 == 0 && a.h0 != nullptr) {  // NEXT-2: state carried into the row
+    const float* hp = a.h0 + ((int64_t)r * Dn + d) * N;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) h[p] = make_float2(__ldg(hp + 2 * p), __ldg(hp + 2 * p + 1));
+  }
 
   // Flat loop over 8-step sub-blocks; u/dt of the next sub-block are loaded
   // into registers before the current one is computed (software pipeline),
   // B/C/head tiles are restaged at every kTile boundary.  Sub-blocks fully
   // inside the segment (all but at most two) run without per-step checks.
   int tb = s0 & ~7;
-  Raw8<T, kVec> pu, pt;
+  Raw8<T, kVec> pu, pt, pz;
   pu.load(u_row, tb, L);
   pt.load(dt_row, tb, L);
+  if (kGate) pz.load(z_row, tb, L);
   int j0 = -1;
   unsigned long long hmask = 0ull;
   for (; tb < s1; tb += 8) {
     if (j0 < 0 || (tb & (kTile - 1)) == 0) {  // CTA-uniform
       j0 = tb & ~(kTile - 1);
       __syncthreads();
-      stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask);
+      stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask, a.h0 == nullptr);
       __syncthreads();
       // head flags of the tile as a register bitmask (CTA-uniform): no
       // shared-memory load on the per-step critical path
       hmask = (unsigned long long)sMask[0] | ((unsigned long long)sMask[1] << 32);
     }
-    float uu[8], vv[8], yy[8];
+    float uu[8], vv[8], yy[8], zz[8];
     pu.unpack(uu);
     pt.unpack(vv);
+    if (kGate) pz.unpack(zz);
     if (tb + 8 < s1) {
       pu.load(u_row, tb + 8, L);
       pt.load(dt_row, tb + 8, L);
+      if (kGate) pz.load(z_row, tb + 8, L);
     }
     const int sb = tb - j0;
     // checkpoint = state before step tb (only step i == 0 can be a multiple of kChunk)
@@ -313,11 +331,20 @@ scan_fwd_kernel(const ScanFwdArgs a) {
         for (int p = 0; p < NP; ++p) yp[p & 1] = ffma2(Ct[p], h[p], yp[p & 1]);
         const float2 ys = fadd2(yp[0], yp[1]);
         yy[i] = ys.x + ys.y;
+        if (kGate) yy[i] *= zz[i] * sigmoidf_fast(zz[i]);  // out = y * silu(z)
       }
     };
     if (tb >= s0 && tb + 8 <= s1) block(std::true_type{});
     else block(std::false_type{});
     if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
+  }
+  if (s1 == L && a.h_last != nullptr && active) {  // state after the row's last step
+    float* hp = a.h_last + ((int64_t)r * Dn + d) * N;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      hp[2 * p] = h[p].x;
+      hp[2 * p + 1] = h[p].y;
+    }
   }
   }  // work loop
 }
@@ -352,25 +379,28 @@ constexpr int kBSub = 2;                     // bwd register sub-chunk (= one re
 constexpr int kBNSub = kChunk / kBSub;
 static_assert(kChunk == 16, "phase 1 maps 8 steps to each thread of a pair");
 
-template <typename T, int N>
+template <typename T, int N, bool kGate>
 struct BwdRaw {  // raw inputs of one chunk, filled by cp.async (vector path)
   T u[kBwdCh][kChunk];
   T dt[kBwdCh][kChunk];
   T dy[kBwdCh][kChunk];
+  T z[kGate ? kBwdCh : 1][kChunk];
   T B[N][kChunk];
   T C[N][kChunk];
   int32_t pos[kChunk];
   float st[N][kBwdCh];
 };
 
-template <typename T, int N>
+template <typename T, int N, bool kGate>
 struct BwdSmem {
   static constexpr int NH = N / 2;   // states per thread
   static constexpr int kQ = N / 4;   // float4 quads of (dB, dC) values per thread-step
   static constexpr int kRows = 2 * kQ;  // transpose rows per 2-step round
-  BwdRaw<T, N> raw;
+  BwdRaw<T, N, kGate> raw;
   float4 sc[kChunk][kBwdCh];  // per-(t,d) scalars {delta, u, dy, softplus'(v)}
-                              // (u = dy = 0 on inactive channels)
+                              // (u = dy = 0 on inactive channels; with the
+                              // gate, dy = dout * silu(z))
+  float sgz[kGate ? kChunk : 1][kBwdCh];  // dout * silu'(z) (gate only)
   float4 red[kBwdWarps][kRows][kRedStride];
   float4 xw[kChunk / 2][kBwdWarps][kRows][2];
   float B[kChunk][N];
@@ -382,22 +412,25 @@ struct BwdSmem {
 
 // Issue the cp.async copies of chunk c's raw inputs (vector path only:
 // L*isz % 16 == 0, Dn % 4 == 0, 16-byte aligned pointers).
-template <typename T, int N>
-PM_DEV void bwd_issue_raw(BwdRaw<T, N>& rw, const ScanBwdArgs& a, int r, int dblk, int c, int s0) {
+template <typename T, int N, bool kGate>
+PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, int dblk, int c,
+                          int s0) {
   constexpr int kEl = 16 / (int)sizeof(T);       // elements per 16-byte chunk
   constexpr int kRowQ = kChunk / kEl;            // chunks per (row, chunk)
   const int L = a.L, Dn = a.Dn, cb = c * kChunk;
-  const T* srcs[3] = {static_cast<const T*>(a.u), static_cast<const T*>(a.dt),
-                      static_cast<const T*>(a.dy)};
-  T(*dsts[3])[kChunk] = {rw.u, rw.dt, rw.dy};
   constexpr int kTx = kBwdCh * kRowQ;
-  for (int e = threadIdx.x; e < 3 * kTx; e += kBwdThreads) {
-    const int arr = e / kTx, rem = e % kTx, ch = rem / kRowQ, q = rem % kRowQ;
-    const int d = dblk * kBwdCh + ch;
-    const int t0 = cb + q * kEl;
-    const bool ok = d < Dn && t0 < L;
-    const T* src = ok ? srcs[arr] + ((int64_t)r * Dn + d) * L + t0 : srcs[arr];
-    cp_async16(&dsts[arr][ch][q * kEl], src, ok ? 16 : 0);
+#pragma unroll
+  for (int arr = 0; arr < (kGate ? 4 : 3); ++arr) {  // u, dt, dy (, z)
+    const T* base = static_cast<const T*>(arr == 0 ? a.u : arr == 1 ? a.dt : arr == 2 ? a.dy : a.z);
+    T(*dst)[kChunk] = arr == 0 ? rw.u : arr == 1 ? rw.dt : arr == 2 ? rw.dy : rw.z;
+    for (int e = threadIdx.x; e < kTx; e += kBwdThreads) {
+      const int ch = e / kRowQ, q = e % kRowQ;
+      const int d = dblk * kBwdCh + ch;
+      const int t0 = cb + q * kEl;
+      const bool ok = d < Dn && t0 < L;
+      const T* src = ok ? base + ((int64_t)r * Dn + d) * L + t0 : base;
+      cp_async16(&dst[ch][q * kEl], src, ok ? 16 : 0);
+    }
   }
   const T* Bp = static_cast<const T*>(a.B) + (int64_t)r * N * L;
   const T* Cp = static_cast<const T*>(a.C) + (int64_t)r * N * L;
@@ -413,7 +446,7 @@ PM_DEV void bwd_issue_raw(BwdRaw<T, N>& rw, const ScanBwdArgs& a, int r, int dbl
     const bool ok = t0 < L;
     cp_async16(&rw.pos[4 * e], a.pos + (int64_t)r * L + (ok ? t0 : 0), ok ? 16 : 0);
   }
-  if (cb > s0) {
+  if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
     for (int e = threadIdx.x; e < N * (kBwdCh / 4); e += kBwdThreads) {
       const int n = e / (kBwdCh / 4), q = e % (kBwdCh / 4);
       const int d0 = dblk * kBwdCh + 4 * q;
@@ -425,11 +458,11 @@ PM_DEV void bwd_issue_raw(BwdRaw<T, N>& rw, const ScanBwdArgs& a, int r, int dbl
   cp_async_commit();
 }
 
-template <typename T, int N, bool kVec, int MinB>
+template <typename T, int N, bool kVec, int MinB, bool kGate>
 __global__ void __launch_bounds__(kBwdThreads, MinB)
 scan_bwd_kernel(const ScanBwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  using SM = BwdSmem<T, N>;
+  using SM = BwdSmem<T, N, kGate>;
   constexpr int NH = SM::NH, kQ = SM::kQ, kRows = SM::kRows;
   SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
@@ -511,7 +544,14 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   float dD = 0.f, ddtb = 0.f;
 
   const int cfirst = s0 / kChunk, clast = (s1 - 1) / kChunk;
-  if constexpr (kVec) bwd_issue_raw<T, N>(sm.raw, a, r, dblk, clast, s0);
+  if constexpr (kVec) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, clast, s0);
+  if (s1 == L && a.dh_last != nullptr) {  // NEXT-2: cotangent of the carried-out state
+    const float* gp = a.dh_last + ((int64_t)r * Dn + d) * N + n0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) g[p] = make_float2(__ldg(gp + 2 * p), __ldg(gp + 2 * p + 1));
+  }
+  const T* z_row = kGate ? static_cast<const T*>(a.z) + lane : nullptr;
+  T* dz_row = kGate ? static_cast<T*>(a.dz) + lane : nullptr;
 
   for (int c = clast; c >= cfirst; --c) {
     const int cb = c * kChunk, c0 = max(cb, s0), c1 = min(cb + kChunk, s1);
@@ -520,7 +560,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     // ---- phase 1: scalars, B/C, head, chunk start state ----
     float2 h[NP];
     {
-      float uu[8], vv[8], yy[8];
+      float uu[8], vv[8], yy[8], zz[8];
       if constexpr (kVec) {
         const T* ru = &sm.raw.u[cl][8 * hf];
         const T* rt = &sm.raw.dt[cl][8 * hf];
@@ -530,11 +570,13 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           uu[i] = IO<T>::cvt(ru[i]);
           vv[i] = IO<T>::cvt(rt[i]);
           yy[i] = IO<T>::cvt(ry[i]);
+          if constexpr (kGate) zz[i] = IO<T>::cvt(sm.raw.z[cl][8 * hf + i]);
         }
       } else {
         load8<T, false>(u_row, cb + 8 * hf, L, uu);
         load8<T, false>(dt_row, cb + 8 * hf, L, vv);
         load8<T, false>(dy_row, cb + 8 * hf, L, yy);
+        if constexpr (kGate) load8<T, false>(z_row, cb + 8 * hf, L, zz);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -546,7 +588,13 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           dl = softplus_x(v, x);
           sg = v > 20.f ? 1.f : __fdividef(x, 1.f + x);
         }
-        sm.sc[ii][cl] = make_float4(dl, active ? uu[i] : 0.f, active ? yy[i] : 0.f, sg);
+        float dyv = yy[i];
+        if constexpr (kGate) {  // out = y silu(z): dy = dout silu(z), dz = dout silu'(z) y
+          const float sz = sigmoidf_fast(zz[i]);
+          dyv = yy[i] * zz[i] * sz;
+          sm.sgz[ii][cl] = active ? yy[i] * sz * fmaf(zz[i], 1.f - sz, 1.f) : 0.f;
+        }
+        sm.sc[ii][cl] = make_float4(dl, active ? uu[i] : 0.f, active ? dyv : 0.f, sg);
       }
       if constexpr (kVec) {
         for (int e = tid; e < N * kChunk; e += kBwdThreads) {
@@ -556,11 +604,12 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         }
         if (tid < 32) {
           const int t = cb + tid;
-          const bool f = tid < kChunk && (t >= L || t == 0 || sm.raw.pos[tid & (kChunk - 1)] == 0);
+          const bool f = tid < kChunk && (t >= L || (t == 0 && a.h0 == nullptr) ||
+                                          sm.raw.pos[tid & (kChunk - 1)] == 0);
           const unsigned m = __ballot_sync(0xffffffffu, f);
           if (tid == 0) sm.hmask[0] = m;
         }
-        if (cb > s0) {
+        if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
 #pragma unroll
           for (int p = 0; p < NP; ++p)
             h[p] = make_float2(sm.raw.st[n0 + 2 * p][cl], sm.raw.st[n0 + 2 * p + 1][cl]);
@@ -569,8 +618,9 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
         }
       } else {
-        stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.hmask);
-        if (cb > s0) {
+        stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.hmask,
+                                      a.h0 == nullptr);
+        if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
           const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
 #pragma unroll
           for (int p = 0; p < NP; ++p)
@@ -584,7 +634,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     __syncthreads();  // scalars visible; raw buffer free
     const uint32_t hmask = sm.hmask[0];  // head flags of the chunk (CTA-uniform register)
     if constexpr (kVec) {
-      if (c > cfirst) bwd_issue_raw<T, N>(sm.raw, a, r, dblk, c - 1, s0);
+      if (c > cfirst) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, c - 1, s0);
     }
 
     auto passes = [&](auto full_tag) {
@@ -650,7 +700,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           }
         }
       }
-      float duo[kBSub], ddo[kBSub];
+      float duo[kBSub], ddo[kBSub], dzo[kBSub];
 #pragma unroll
       for (int i = kBSub - 1; i >= 0; --i) {
         const int t = a0 + i, ii = t - cb;
@@ -661,6 +711,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           for (int q = 0; q < kQ; ++q) rslot(q) = make_float4(0.f, 0.f, 0.f, 0.f);
           duo[i] = 0.f;
           ddo[i] = 0.f;
+          dzo[i] = 0.f;
           continue;
         }
         const float4 scv = sm.sc[ii][cl];
@@ -686,6 +737,14 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           g[p] = fmul2(ab[i][p], g[p]);  // carry to t-1 (0 at heads)
         }
         float Ssum = Sp.x + Sp.y, dq = dqp.x + dqp.y;
+        if constexpr (kGate) {  // y_t = C_t . h_t + D u_t (pre-gate) for dz
+          float2 yp = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) yp = ffma2(Ct[p], hb[i][p], yp);
+          float yv = yp.x + yp.y;
+          yv += __shfl_xor_sync(0xffffffffu, yv, 1);
+          dzo[i] = fmaf(Dd, ux, yv) * sm.sgz[ii][cl];
+        }
 #pragma unroll
         for (int q = 0; q < kQ; ++q)
           rslot(q) = make_float4(vals[2 * q].x, vals[2 * q].y, vals[2 * q + 1].x, vals[2 * q + 1].y);
@@ -727,9 +786,11 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         if (kFull) {
           store2<T, kVec>(du_row, a0, a0, a0 + kBSub, duo);
           store2<T, kVec>(ddt_row, a0, a0, a0 + kBSub, ddo);
+          if constexpr (kGate) store2<T, kVec>(dz_row, a0, a0, a0 + kBSub, dzo);
         } else {
           store2<T, kVec>(du_row, a0, c0, c1, duo);
           store2<T, kVec>(ddt_row, a0, c0, c1, ddo);
+          if constexpr (kGate) store2<T, kVec>(dz_row, a0, c0, c1, dzo);
         }
       }
     };
@@ -774,6 +835,14 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     if (hf == 0) {
       wsp[(int64_t)N * Dn + d] = dD;
       wsp[(int64_t)(N + 1) * Dn + d] = ddtb;
+    }
+    if (s0 == 0 && a.dh0 != nullptr) {  // NEXT-2: g now holds abar_0 g_0 = dL/dh0
+      float* gp = a.dh0 + ((int64_t)r * Dn + d) * N + n0;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        gp[2 * p] = g[p].x;
+        gp[2 * p + 1] = g[p].y;
+      }
     }
   }
   }  // work loop
@@ -883,14 +952,6 @@ bool elem_aligned(const void* p, pm_dtype io) {
   return p == nullptr || (reinterpret_cast<uintptr_t>(p) & m) == 0;
 }
 
-// Occupancy variants (min resident CTAs per SM -> register cap).  The
-// default is the measured best on B200; PM_TUNE_FWD_MINB / PM_TUNE_BWD_MINB
-// override it for tuning sweeps (read per call; no global state).
-int tune_env(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
-
 // persistent grid: resident CTAs on all SMs, capped by the number of items
 template <typename K>
 int persistent_grid(K kern, int threads, size_t smem, int64_t items) {
@@ -905,9 +966,9 @@ int persistent_grid(K kern, int threads, size_t smem, int64_t items) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, items));
 }
 
-template <typename T, int N, bool kVec, int MinB>
+template <typename T, int N, bool kVec, int MinB, bool kGate>
 void fwd_go(const ScanFwdArgs& a, cudaStream_t s) {
-  auto kern = scan_fwd_kernel<T, N, kVec, MinB>;
+  auto kern = scan_fwd_kernel<T, N, kVec, MinB, kGate>;
   if (a.items != nullptr) {
     const int g = persistent_grid(kern, kScanThreads, 0, (int64_t)a.n_items * n_dblk(a.Dn));
     kern<<<g, kScanThreads, 0, s>>>(a);
@@ -926,12 +987,8 @@ pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
     seg_sort_kernel<<<1, 1024, 0, s>>>(sc.unsorted, a.n_items, a.L, sc.sorted);
     PM_LAUNCH_CHECK();
   }
-  switch (tune_env("PM_TUNE_FWD_MINB", kFwdMinB)) {
-    case 3: fwd_go<T, N, kVec, 3>(a, s); break;
-    case 5: fwd_go<T, N, kVec, 5>(a, s); break;
-    case 6: fwd_go<T, N, kVec, 6>(a, s); break;
-    default: fwd_go<T, N, kVec, 4>(a, s); break;
-  }
+  if (a.z != nullptr) fwd_go<T, N, kVec, kFwdMinB, true>(a, s);
+  else fwd_go<T, N, kVec, kFwdMinB, false>(a, s);
   PM_LAUNCH_CHECK();
   return PM_OK;
 }
@@ -950,12 +1007,10 @@ pm_status dispatch_fwd(const ScanFwdArgs& a, int N, bool vec, cudaStream_t s) {
   }
 }
 
-template <typename T, int N, bool kVec>
-pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, float* dD,
-                     float* ddtb, cudaStream_t s) {
-  const size_t smem = sizeof(BwdSmem<T, N>);
-  auto kern = tune_env("PM_TUNE_BWD_MINB", kBwdMinB) == 3 ? scan_bwd_kernel<T, N, kVec, 3>
-                                                          : scan_bwd_kernel<T, N, kVec, 4>;
+template <typename T, int N, bool kVec, bool kGate>
+pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
+  const size_t smem = sizeof(BwdSmem<T, N, kGate>);
+  auto kern = scan_bwd_kernel<T, N, kVec, kBwdMinB, kGate>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return PM_ERR_CUDA;
   // prefer the maximum shared-memory carveout so 4 CTAs (54 KB each) fit per SM
@@ -970,8 +1025,7 @@ pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, floa
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int minb = tune_env("PM_TUNE_BWD_MINB", kBwdMinB) == 3 ? 3 : 4;
-    const int nb = std::max(1, std::min<int>(minb, (int)((228 * 1024) / (smem + 1024))));
+    const int nb = std::max(1, std::min<int>(kBwdMinB, (int)((228 * 1024) / (smem + 1024))));
     const int64_t items = (int64_t)a.n_items * n_dblk_bwd(a.Dn);
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * nb, items));
     if (getenv("PM_DEBUG"))
@@ -981,6 +1035,15 @@ pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, floa
     kern<<<dim3(n_dblk_bwd(a.Dn), a.R, a.nseg), kBwdThreads, smem, s>>>(a);
   }
   PM_LAUNCH_CHECK();
+  return PM_OK;
+}
+
+template <typename T, int N, bool kVec>
+pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, float* dD,
+                     float* ddtb, cudaStream_t s) {
+  const pm_status st = a.z != nullptr ? launch_bwd_k<T, N, kVec, true>(a, s)
+                                      : launch_bwd_k<T, N, kVec, false>(a, s);
+  if (st != PM_OK) return st;
   dim3 g2((a.L + 31) / 32, a.R);
   scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
   PM_LAUNCH_CHECK();
@@ -1035,24 +1098,27 @@ size_t pm_selective_scan_bwd_workspace(int64_t R, int64_t Dn, int64_t L, int32_t
   return bwd_ws_bytes(R, Dn, L, N, recompute_states != 0);
 }
 
-pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, const void* B,
-                                const void* C, const float* Dskip, const float* dt_bias,
-                                int32_t dt_softplus, const int32_t* pos, void* y, float* states,
-                                int64_t R, int64_t Dn, int64_t L, int32_t N, pm_dtype io,
-                                pm_stream_t stream) {
+pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt, const float* A,
+                                   const void* B, const void* C, const float* Dskip,
+                                   const float* dt_bias, int32_t dt_softplus, const int32_t* pos,
+                                   const void* z, const float* h0, void* out, float* states,
+                                   float* h_last, int64_t R, int64_t Dn, int64_t L, int32_t N,
+                                   pm_dtype io, pm_stream_t stream) {
   pm_status st = check_common(R, Dn, L, N, io);
   if (st != PM_OK) return st;
-  if (!u || !dt || !A || !B || !C || !pos || (!y && !states)) return PM_ERR_INVALID_ARG;
-  for (const void* p : {u, dt, B, C, (const void*)y})
+  if (!u || !dt || !A || !B || !C || !pos || (!out && !states && !h_last)) return PM_ERR_INVALID_ARG;
+  for (const void* p : {u, dt, B, C, z, (const void*)out})
     if (!elem_aligned(p, io)) return PM_ERR_ALIGN;
-  for (const void* p : {(const void*)A, (const void*)Dskip, (const void*)dt_bias, (const void*)pos})
+  for (const void* p : {(const void*)A, (const void*)Dskip, (const void*)dt_bias, (const void*)pos,
+                        (const void*)h0, (const void*)h_last})
     if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
   if (!aligned16(states)) return PM_ERR_ALIGN;
   const int isz = io == PM_F32 ? 4 : 2;
   const bool vec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
-                   aligned16(C) && aligned16(y);
-  ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, y, states, nullptr, nullptr, 0,
-                (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0};
+                   aligned16(C) && aligned16(out) && aligned16(z);
+  ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, out, states, nullptr, nullptr, 0,
+                (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
+                z, h0, h_last};
   if (states != nullptr) {  // persistent longest-first schedule lives in the states buffer
     Sched sc = sched_of(states, R, Dn, L, N);
     a.items = sc.sorted;
@@ -1063,30 +1129,44 @@ pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, c
   return io == PM_F32 ? dispatch_fwd<float>(a, N, vec, s) : dispatch_fwd<__nv_bfloat16>(a, N, vec, s);
 }
 
-pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, const void* B,
+pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, const void* B,
                                 const void* C, const float* Dskip, const float* dt_bias,
-                                int32_t dt_softplus, const int32_t* pos, const float* states,
-                                const void* dy, void* du, void* ddt, float* dA, float* dB,
-                                float* dC, float* dD, float* ddt_bias, void* workspace,
-                                size_t ws_bytes, int64_t R, int64_t Dn, int64_t L, int32_t N,
-                                pm_dtype io, pm_stream_t stream) {
+                                int32_t dt_softplus, const int32_t* pos, void* y, float* states,
+                                int64_t R, int64_t Dn, int64_t L, int32_t N, pm_dtype io,
+                                pm_stream_t stream) {
+  if (!y && !states) return PM_ERR_INVALID_ARG;
+  return pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, pos, nullptr,
+                                  nullptr, y, states, nullptr, R, Dn, L, N, io, stream);
+}
+
+pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A, const void* B,
+                                   const void* C, const float* Dskip, const float* dt_bias,
+                                   int32_t dt_softplus, const int32_t* pos, const void* z,
+                                   const float* h0, const float* states, const void* dout,
+                                   const float* dh_last, void* du, void* ddt, float* dA,
+                                   float* dB, float* dC, float* dD, float* ddt_bias, void* dz,
+                                   float* dh0, void* workspace, size_t ws_bytes, int64_t R,
+                                   int64_t Dn, int64_t L, int32_t N, pm_dtype io,
+                                   pm_stream_t stream) {
   pm_status st = check_common(R, Dn, L, N, io);
   if (st != PM_OK) return st;
-  if (!u || !dt || !A || !B || !C || !pos || !dy || !du || !ddt || !dA || !dB || !dC)
+  if (!u || !dt || !A || !B || !C || !pos || !dout || !du || !ddt || !dA || !dB || !dC ||
+      (z != nullptr) != (dz != nullptr))
     return PM_ERR_INVALID_ARG;
   const bool recompute = states == nullptr;
   if (!workspace || ws_bytes < bwd_ws_bytes(R, Dn, L, N, recompute)) return PM_ERR_WORKSPACE;
   if (!aligned16(workspace) || !aligned16(states)) return PM_ERR_ALIGN;
-  for (const void* p : {u, dt, B, C, dy, (const void*)du, (const void*)ddt})
+  for (const void* p : {u, dt, B, C, z, dout, (const void*)du, (const void*)ddt, (const void*)dz})
     if (!elem_aligned(p, io)) return PM_ERR_ALIGN;
   for (const void* p : {(const void*)A, (const void*)Dskip, (const void*)dt_bias, (const void*)pos,
                         (const void*)dA, (const void*)dB, (const void*)dC, (const void*)dD,
-                        (const void*)ddt_bias})
+                        (const void*)ddt_bias, (const void*)h0, (const void*)dh_last,
+                        (const void*)dh0})
     if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
   const int isz = io == PM_F32 ? 4 : 2;
   const bool vec = (L * isz) % 16 == 0 && Dn % 4 == 0 && aligned16(u) && aligned16(dt) &&
-                   aligned16(B) && aligned16(C) && aligned16(dy) && aligned16(du) &&
-                   aligned16(ddt);
+                   aligned16(B) && aligned16(C) && aligned16(dout) && aligned16(du) &&
+                   aligned16(ddt) && aligned16(z) && aligned16(dz);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(workspace);
   float* ws_bc = reinterpret_cast<float*>(w);
@@ -1099,7 +1179,8 @@ pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, c
   if (recompute) {
     float* st_ws = reinterpret_cast<float*>(w);
     ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws, nullptr, nullptr, 0,
-                   (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0};
+                   (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
+                   nullptr, h0, nullptr};
     Sched sc = sched_of(st_ws, R, Dn, L, N);
     fa.items = sc.sorted;
     fa.counter = sc.counters;
@@ -1113,11 +1194,24 @@ pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, c
   }
   // the length-sorted segment list written by the forward pass
   const Sched sc = sched_of(const_cast<float*>(stp), R, Dn, L, N);
-  ScanBwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, stp, dy, du, ddt, ws_bc, ws_par,
+  ScanBwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, stp, dout, du, ddt, ws_bc, ws_par,
                 sc.sorted, counter, (int)(R * n_seg(L)),
-                (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0};
+                (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
+                z, h0, dh_last, dz, dh0};
   return io == PM_F32 ? dispatch_bwd<float>(a, N, vec, dA, dB, dC, dD, ddt_bias, s)
                       : dispatch_bwd<__nv_bfloat16>(a, N, vec, dA, dB, dC, dD, ddt_bias, s);
+}
+
+pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, const void* B,
+                                const void* C, const float* Dskip, const float* dt_bias,
+                                int32_t dt_softplus, const int32_t* pos, const float* states,
+                                const void* dy, void* du, void* ddt, float* dA, float* dB,
+                                float* dC, float* dD, float* ddt_bias, void* workspace,
+                                size_t ws_bytes, int64_t R, int64_t Dn, int64_t L, int32_t N,
+                                pm_dtype io, pm_stream_t stream) {
+  return pm_selective_scan_bwd_ex(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, pos, nullptr,
+                                  nullptr, states, dy, nullptr, du, ddt, dA, dB, dC, dD, ddt_bias,
+                                  nullptr, nullptr, workspace, ws_bytes, R, Dn, L, N, io, stream);
 }
 
 }  // extern "C"

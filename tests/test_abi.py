@@ -88,6 +88,23 @@ def test_validation_before_launch():
     # bf16: odd address is misaligned, even is fine for validation
     assert L.pm_selective_scan_fwd(_vp(0x1001), *([p] * 6), 1, p, p, p, 2, 8, 64, 16, 1,
                                    None) == 5
+    # extended scan: z requires dz (and vice versa); out/states/h_last all NULL
+    ex_f = lambda *a: L.pm_selective_scan_fwd_ex(*a)
+    assert ex_f(*([p] * 7), 1, p, None, None, None, None, None, 2, 8, 64, 16, 0, None) == 1
+    assert ex_f(*([p] * 7), 1, p, _vp(0x1002), None, p, None, None, 2, 8, 64, 16, 0, None) == 5
+    ebase = [p] * 7 + [1, p]
+    tail = [ws, 2, 8, 64, 16, 0, None]
+    # z given, dz missing
+    assert L.pm_selective_scan_bwd_ex(*ebase, p, None, p, p, None, *([p] * 7), None, None,
+                                      p, *tail) == 1
+    # dz given, z missing
+    assert L.pm_selective_scan_bwd_ex(*ebase, None, None, p, p, None, *([p] * 7), p, None,
+                                      p, *tail) == 1
+    # misaligned h0 / dh_last / dh0 (fp32)
+    assert L.pm_selective_scan_bwd_ex(*ebase, None, _vp(0x1001), p, p, None, *([p] * 7), None,
+                                      None, p, *tail) == 5
+    assert L.pm_selective_scan_bwd_ex(*ebase, None, None, p, p, _vp(0x1002), *([p] * 7), None,
+                                      None, p, *tail) == 5
     # state bytes: (R, ceil(L/16), N, Dn) fp32 states (256-B aligned) + the
     # segment schedule (256 B counters + 2 lists of R*nseg int4, 256-B aligned)
     up = lambda x: (x + 255) // 256 * 256

@@ -1,0 +1,149 @@
+"""GPU parity of the extended scan (SURVEY §8(f) NEXT-1 fused gate + last
+state, NEXT-2 cross-row state passing h0 -> h_last) against the fp64
+oracle's scan_fwd_ext / scan_bwd_ext, through the C ABI
+(pm_selective_scan_fwd_ex / pm_selective_scan_bwd_ex)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+import paper_2408_03865_b200 as pm
+import workload
+from tests._common import TOL, layout, rel_err, to_np
+
+pytestmark = pytest.mark.gpu
+
+DT = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def problem(R, Dn, L, N, kind, io, seed, continued=(), dev="cuda"):
+    """Seeded inputs; rows listed in ``continued`` start mid-sequence: their
+    first sequence's positions are offset so slot 0 is not a head."""
+    rng = np.random.default_rng(seed)
+    rows = layout(kind, R, L, rng)
+    pos_np, valid = workload.pos_from_rows(rows, L)
+    for r in continued:
+        n0 = rows[r][0]
+        pos_np[r, :n0] += 1 + int(rng.integers(0, 500))
+    shape = workload.Shape(f"e{seed}", R, L, Dn, N, 4, io)
+    T = workload.row_tensors(torch, shape, list(range(R)), valid, device=dev, dtype=DT[io])
+    P = workload.params(torch, shape, device=dev)
+    g = torch.Generator().manual_seed(seed)
+    z = torch.randn((R, Dn, L), generator=g).to(dev, DT[io])
+    h0 = torch.randn((R, Dn, N), generator=g).to(dev)
+    dh = torch.randn((R, Dn, N), generator=g).to(dev)
+    # the scan input u: the conv output's range (silu of a unit normal)
+    u = torch.nn.functional.silu(torch.randn((R, Dn, L), generator=g)).to(dev, DT[io])
+    pos = torch.as_tensor(pos_np, device=dev)
+    return pos, u, T, P, z, h0, dh
+
+
+def run_ext(pos, u, T, P, z, h0, dh, states=True):
+    out, st, hl = pm.pm_selective_scan_fwd_ex(u, T["dt"], P["A"], T["B"], T["C"], P["D"],
+                                               P["dt_bias"], pos, z=z, h0=h0,
+                                               want_states=states, want_last_state=True)
+    g = pm.pm_selective_scan_bwd_ex(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
+                                    pos, T["dy"], z=z, h0=h0, states=st, dh_last=dh,
+                                    want_dh0=True)
+    torch.cuda.synchronize()
+    return out, hl, g
+
+
+def check_ext(pos, u, T, P, z, h0, dh, io, res):
+    out, hl, g = res
+    args = (to_np(u), to_np(T["dt"]), to_np(P["A"]), to_np(T["B"]), to_np(T["C"]),
+            to_np(P["D"]), to_np(P["dt_bias"]), to_np(pos).astype(np.int32))
+    zz, hh = to_np(z), to_np(h0)
+    ro, rhl = oracle.scan_fwd_ext(*args, z=zz, h0=hh)
+    ref = oracle.scan_bwd_ext(*args, to_np(T["dy"]), z=zz, h0=hh, dh_last=to_np(dh))
+    errs = {"out": (rel_err(to_np(out), ro), "fwd"), "h_last": (rel_err(to_np(hl), rhl), "fwd")}
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dz", "dh0"):
+        if ref.get(k) is not None and g.get(k) is not None:
+            errs[k] = (rel_err(to_np(g[k]), ref[k]), "bwd")
+    bad = {k: (e, TOL[(io, kind)]) for k, (e, kind) in errs.items() if not e <= TOL[(io, kind)]}
+    assert not bad, f"tolerance exceeded: {bad}; all: {errs}"
+    return errs
+
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+@pytest.mark.parametrize("kind", ["random", "one", "edges"])
+def test_ext_gate_and_state_passing(io, kind):
+    pos, u, T, P, z, h0, dh = problem(3, 200, 1024, 16, kind, io, seed=40 + len(kind),
+                                      continued=(0, 2))
+    check_ext(pos, u, T, P, z, h0, dh, io, run_ext(pos, u, T, P, z, h0, dh))
+
+
+@pytest.mark.parametrize("N", [4, 8])
+@pytest.mark.parametrize("L", [13, 700])
+def test_ext_shapes_and_scalar_path(N, L):
+    pos, u, T, P, z, h0, dh = problem(2, 70, L, N, "random", "f32", seed=N * 1000 + L,
+                                      continued=(1,))
+    check_ext(pos, u, T, P, z, h0, dh, "f32", run_ext(pos, u, T, P, z, h0, dh))
+
+
+def test_ext_each_option_alone():
+    """z only, h0 only, dh_last only: each against the oracle."""
+    pos, u, T, P, z, h0, dh = problem(2, 64, 512, 16, "random", "f32", seed=7, continued=(0,))
+    for zz, hh, dd in ((z, None, None), (None, h0, None), (None, None, dh)):
+        res = run_ext(pos, u, T, P, zz, hh, dd)
+        out, hl, g = res
+        args = (to_np(u), to_np(T["dt"]), to_np(P["A"]), to_np(T["B"]), to_np(T["C"]),
+                to_np(P["D"]), to_np(P["dt_bias"]), to_np(pos).astype(np.int32))
+        ro, rhl = oracle.scan_fwd_ext(*args, z=to_np(zz), h0=to_np(hh))
+        ref = oracle.scan_bwd_ext(*args, to_np(T["dy"]), z=to_np(zz), h0=to_np(hh),
+                                  dh_last=to_np(dd))
+        assert rel_err(to_np(out), ro) <= 1e-4
+        assert rel_err(to_np(hl), rhl) <= 1e-4
+        for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dz", "dh0"):
+            if ref.get(k) is not None and g.get(k) is not None:
+                assert rel_err(to_np(g[k]), ref[k]) <= 1e-3, k
+
+
+def test_ext_without_options_equals_base_abi():
+    """pm_selective_scan_*_ex with no options is the base ABI, bit for bit."""
+    pos, u, T, P, z, h0, dh = problem(2, 96, 900, 16, "random", "bf16", seed=8)
+    y, st = pm.pm_selective_scan_fwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
+                                     pos)
+    g = pm.pm_selective_scan_bwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos,
+                                 T["dy"], states=st)
+    out, hl, ge = run_ext(pos, u, T, P, None, None, None)
+    assert torch.equal(out, y)
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias"):
+        assert torch.equal(ge[k], g[k]), k
+    assert ge["dz"] is None
+
+
+def test_ext_recompute_states_equals_saved():
+    pos, u, T, P, z, h0, dh = problem(2, 96, 900, 16, "random", "f32", seed=9, continued=(1,))
+    a = run_ext(pos, u, T, P, z, h0, dh, states=True)
+    b = run_ext(pos, u, T, P, z, h0, dh, states=False)
+    assert torch.equal(a[0], b[0])
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dz", "dh0"):
+        assert torch.equal(a[2][k], b[2][k]), k
+
+
+@pytest.mark.parametrize("m", [16, 333, 512])
+def test_cut_row_state_passing_reproduces_uncut(m):
+    """a row cut at slot m into two rows with h_last -> h0 (and dh0 ->
+    dh_last backwards) gives the uncut row's results; per-token outputs are
+    bit-identical (the per-lane recurrence runs the same operations in the
+    same order), per-parameter sums agree to rounding."""
+    L = 1024
+    pos, u, T, P, z, h0, dh = problem(1, 128, L, 16, "random", "f32", seed=11 + m)
+    full = run_ext(pos, u, T, P, z, None, None)
+    cut = lambda t, s: t[..., s].contiguous()
+    a1, a2 = slice(0, m), slice(m, L)
+
+    def part(s, h0_, dh_):
+        Tp = {k: cut(T[k], s) for k in ("dt", "B", "C", "dy")}
+        return run_ext(cut(pos, s), cut(u, s), Tp, P, cut(z, s), h0_, dh_)
+
+    o1, hl1, _ = part(a1, None, None)
+    o2, _, g2 = part(a2, hl1, None)
+    _, _, g1 = part(a1, None, g2["dh0"])
+    assert torch.equal(torch.cat([o1, o2], -1), full[0])
+    for k in ("du", "ddt", "dz", "dB", "dC"):
+        assert torch.equal(torch.cat([g1[k], g2[k]], -1), full[2][k]), k
+    for k in ("dA", "dD", "ddt_bias"):
+        torch.testing.assert_close(g1[k] + g2[k], full[2][k], rtol=1e-5, atol=1e-5)
