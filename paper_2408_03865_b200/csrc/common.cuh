@@ -259,10 +259,24 @@ PM_DEV void tmem_st(uint32_t taddr, const float* v) {
   }
 }
 
-template <int M>  // load M values from columns [c, c+M) of my lane (call tmem_wait_ld before use)
+template <int M>  // load M (2..32, power of 2) values from columns [c, c+M) of my lane, then wait
 PM_DEV void tmem_ld(uint32_t taddr, float* v) {
-  uint32_t r[8];
-  if constexpr (M == 8) {
+  static_assert(M == 2 || M == 4 || M == 8 || M == 16 || M == 32, "M in {2, 4, 8, 16, 32}");
+  uint32_t r[M];
+  if constexpr (M == 32) {
+    tmem_ld<16>(taddr, v);
+    tmem_ld<16>(taddr + 16, v + 16);
+    return;
+  } else if constexpr (M == 16) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+  } else if constexpr (M == 8) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
                    "=r"(r[7])
@@ -274,7 +288,6 @@ PM_DEV void tmem_ld(uint32_t taddr, float* v) {
                  : "r"(taddr)
                  : "memory");
   } else {
-    static_assert(M == 2, "M in {2, 4, 8}");
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n"
                  : "=r"(r[0]), "=r"(r[1])
                  : "r"(taddr)
@@ -282,7 +295,10 @@ PM_DEV void tmem_ld(uint32_t taddr, float* v) {
   }
   tmem_wait_ld();
 #pragma unroll
-  for (int k = 0; k < M; ++k) v[k] = __uint_as_float(r[k]);
+  for (int k = 0; k < M; ++k) {
+    asm volatile("" : "+r"(r[k]));  // keep every use of the value after the wait
+    v[k] = __uint_as_float(r[k]);
+  }
 }
 
 // --------------------------------------------------- segment splitting ----

@@ -471,9 +471,10 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   const int cl = tid >> 1, hf = tid & 1;
   const int n0 = hf * NH;  // first state of this thread
   const int ndblk = (Dn + kBwdCh - 1) / kBwdCh;
-  // sub-chunk start states live in tensor memory (one TMEM lane per thread,
-  // kBNSub * NH fp32 columns), freeing shared memory for a 4th CTA per SM.
-  constexpr uint32_t kTmemCols = (kBNSub * NH <= 32) ? 32u : (kBNSub * NH <= 64 ? 64u : 128u);
+  // the chunk's per-step states live in tensor memory (one TMEM lane per
+  // thread, kChunk * NH fp32 columns: 128 at N = 16, so 4 CTAs fill the
+  // SM's 512 columns) instead of registers or shared memory.
+  constexpr uint32_t kTmemCols = (kChunk * NH <= 32) ? 32u : (kChunk * NH <= 64 ? 64u : 128u);
   if (wid == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
   tmem_fence_before();
   __syncthreads();
@@ -639,11 +640,11 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 
     auto passes = [&](auto full_tag) {
       constexpr bool kFull = decltype(full_tag)::value;
-    // ---- pass A: forward over the chunk, record sub-chunk start states ----
+    // ---- pass A: forward over the chunk; the state entering step ii is kept
+    //      in TMEM columns [ii*NH, ii*NH + NH) of my lane ----
     auto stepA = [&](const int ii) {
       const int t = cb + ii;
-      if (ii % kBSub == 0)
-        tmem_st<NH>(tbase + (uint32_t)((ii / kBSub) * NH), reinterpret_cast<const float*>(h));
+      tmem_st<NH>(tbase + (uint32_t)(ii * NH), reinterpret_cast<const float*>(h));
       if (!kFull && (t < c0 || t >= c1)) return;  // CTA-uniform
       const float4 scv = sm.sc[ii][cl];
       const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
@@ -663,42 +664,21 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 #pragma unroll 1
       for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
     }
-    tmem_wait_st();  // sub-chunk states are in TMEM before pass B reads them
-    // ---- pass B: 2-step sub-chunks in reverse (= one reduction round);
-    //      fully unrolled on the full-chunk path so every shared-memory and
-    //      TMEM offset is an immediate ----
+    tmem_wait_st();  // states are in TMEM before pass B reads them
+    // ---- pass B: reverse over 2-step rounds (= one reduction round).  h
+    //      holds the state after the round's last step; the states entering
+    //      its steps come from TMEM, so nothing is recomputed forward:
+    //        g += C dy;  S += g B;  dB <- g du;  dC <- dy h_t;
+    //        g <- abar_t g  (carry, 0 at heads);  q = g h_{t-1}  (= g_t abar_t h_{t-1})
+    //        dA += delta q;  dq += A q ----
     auto sub_chunk = [&](const int sc) {
       const int a0 = cb + sc * kBSub;
-      if (!kFull && (a0 >= c1 || a0 + kBSub <= c0)) return;  // CTA-uniform
-      float2 hb[kBSub][NP], ab[kBSub][NP];
-      tmem_ld<NH>(tbase + (uint32_t)(sc * NH), reinterpret_cast<float*>(h));
+      float2 hp[kBSub][NP];  // states entering steps a0 .. a0+kBSub-1
+      tmem_ld<kBSub * NH>(tbase + (uint32_t)(sc * kBSub * NH), reinterpret_cast<float*>(hp));
+      if (!kFull && (a0 >= c1 || a0 + kBSub <= c0)) {  // CTA-uniform
 #pragma unroll
-      for (int i = 0; i < kBSub; ++i) {
-        const int t = a0 + i, ii = t - cb;
-        if (kFull || (t >= c0 && t < c1)) {  // CTA-uniform
-          const float4 scv = sm.sc[ii][cl];
-          const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
-          const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
-          if ((hmask >> ii) & 1u) {
-#pragma unroll
-            for (int p = 0; p < NP; ++p) {
-              ab[i][p] = make_float2(0.f, 0.f);
-              hb[i][p] = fmul2(dux2, Bt[p]);
-            }
-          } else {
-#pragma unroll
-            for (int p = 0; p < NP; ++p) {
-              ab[i][p] = ex2x2(fmul2(dl2, A2[p]));
-              hb[i][p] = ffma2(ab[i][p], i == 0 ? h[p] : hb[i - 1][p], fmul2(dux2, Bt[p]));
-            }
-          }
-        } else {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            ab[i][p] = make_float2(0.f, 0.f);
-            hb[i][p] = i == 0 ? h[p] : hb[i - 1][p];
-          }
-        }
+        for (int p = 0; p < NP; ++p) h[p] = hp[0][p];
+        return;
       }
       float duo[kBSub], ddo[kBSub], dzo[kBSub];
 #pragma unroll
@@ -706,6 +686,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         const int t = a0 + i, ii = t - cb;
         // row (i*kQ + q), column lid: row-wise writes are conflict-free
         auto rslot = [&](int q) -> float4& { return sm.red[wid][i * kQ + q][lid]; };
+        const float2* hc = i == kBSub - 1 ? h : hp[i + 1];  // state after step t
         if (!kFull && (t < c0 || t >= c1)) {  // CTA-uniform
 #pragma unroll
           for (int q = 0; q < kQ; ++q) rslot(q) = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -716,31 +697,38 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         }
         const float4 scv = sm.sc[ii][cl];
         const float delta = scv.x, ux = scv.y, dyv = scv.z;
-        const float dux = delta * ux;
-        const float2 dl2 = f2(delta), dux2 = f2(dux), ndux2 = f2(-dux), dy2 = f2(dyv);
-        const bool head = (hmask >> ii) & 1u;
+        const float2 dl2 = f2(delta), dux2 = f2(delta * ux), dy2 = f2(dyv);
         const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
         const float2* Ct = reinterpret_cast<const float2*>(&sm.C[ii][n0]);
         float2 Sp = make_float2(0.f, 0.f), dqp = make_float2(0.f, 0.f);
         float2 vals[2 * NP];  // [dB of my NH states | dC of my NH states]
+        if ((hmask >> ii) & 1u) {  // head: abar = 0, no carry, no dA / dq term
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          g[p] = ffma2(Ct[p], dy2, g[p]);  // g holds abar_{t+1} g_{t+1}
-          Sp = ffma2(g[p], Bt[p], Sp);
-          // abar_t h_{t-1} = h_t - dux B  (0 at heads: post-reset abar, Q16)
-          const float2 hm = head ? make_float2(0.f, 0.f) : ffma2(ndux2, Bt[p], hb[i][p]);
-          const float2 q = fmul2(g[p], hm);
-          dA[p] = ffma2(dl2, q, dA[p]);
-          dqp = ffma2(A2[p], q, dqp);
-          vals[p] = fmul2(g[p], dux2);
-          vals[NP + p] = fmul2(dy2, hb[i][p]);
-          g[p] = fmul2(ab[i][p], g[p]);  // carry to t-1 (0 at heads)
+          for (int p = 0; p < NP; ++p) {
+            g[p] = ffma2(Ct[p], dy2, g[p]);
+            Sp = ffma2(g[p], Bt[p], Sp);
+            vals[p] = fmul2(g[p], dux2);
+            vals[NP + p] = fmul2(dy2, hc[p]);
+            g[p] = make_float2(0.f, 0.f);
+          }
+        } else {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            g[p] = ffma2(Ct[p], dy2, g[p]);
+            Sp = ffma2(g[p], Bt[p], Sp);
+            vals[p] = fmul2(g[p], dux2);
+            vals[NP + p] = fmul2(dy2, hc[p]);
+            g[p] = fmul2(ex2x2(fmul2(dl2, A2[p])), g[p]);  // carry to t-1
+            const float2 q = fmul2(g[p], hp[i][p]);
+            dA[p] = ffma2(dl2, q, dA[p]);
+            dqp = ffma2(A2[p], q, dqp);
+          }
         }
         float Ssum = Sp.x + Sp.y, dq = dqp.x + dqp.y;
         if constexpr (kGate) {  // y_t = C_t . h_t + D u_t (pre-gate) for dz
           float2 yp = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int p = 0; p < NP; ++p) yp = ffma2(Ct[p], hb[i][p], yp);
+          for (int p = 0; p < NP; ++p) yp = ffma2(Ct[p], hc[p], yp);
           float yv = yp.x + yp.y;
           yv += __shfl_xor_sync(0xffffffffu, yv, 1);
           dzo[i] = fmaf(Dd, ux, yv) * sm.sgz[ii][cl];
@@ -755,6 +743,8 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         dD = fmaf(dyv, ux, dD);
         ddtb += ddo[i];
       }
+#pragma unroll
+      for (int p = 0; p < NP; ++p) h[p] = hp[0][p];
       // warp transpose-reduce of the round: lane -> (row, half, column half)
       __syncwarp();
       {
