@@ -75,9 +75,9 @@ def lib():
                                                      _i64, _i64, _i32]
         L.pmo_seq_scan_bwd.argtypes = ([_f64p] * 7 + [_i32] + [_f64p] * 8 +
                                        [_i64, _i64, _i32])
-        L.pmo_scan_fwd_ext.argtypes = ([_f64p] * 7 + [_i32, _i32p, _f64p, _f64p, _f64p, _f64p,
+        L.pmo_scan_fwd_ext.argtypes = ([_f64p] * 7 + [_i32, _i32, _i32p, _f64p, _f64p, _f64p, _f64p,
                                         _i64, _i64, _i64, _i32])
-        L.pmo_scan_bwd_ext.argtypes = ([_f64p] * 7 + [_i32, _i32p] + [_f64p] * 13 +
+        L.pmo_scan_bwd_ext.argtypes = ([_f64p] * 7 + [_i32, _i32, _i32p] + [_f64p] * 13 +
                                        [_i64, _i64, _i64, _i32])
         L.pmo_num_threads.restype = ctypes.c_int
         L.pmo_set_num_threads.argtypes = [ctypes.c_int]
@@ -288,9 +288,10 @@ def seq_scan_bwd(u, dt, A, B, C, D, dt_bias, dy, acc, softplus=True):
 
 # --- NEXT-1 / NEXT-2: gate and state passing ---------------------------------
 
-def scan_fwd_ext(u, dt, A, B, C, D, dt_bias, pos, z=None, h0=None, softplus=True):
+def scan_fwd_ext(u, dt, A, B, C, D, dt_bias, pos, z=None, h0=None, softplus=True, zoh=False):
     """Returns (out, h_last): out = y * silu(z) (y if z is None); h0 (R,Dn,N)
-    is the state entering t=0 when pos[r,0] != 0."""
+    is the state entering t=0 when pos[r,0] != 0; zoh selects Eq 2b
+     for B-bar instead of Euler."""
     u, dt, A, B, C = _f64(u), _f64(dt), _f64(A), _f64(B), _f64(C)
     D, dt_bias, z, h0 = _f64(D), _f64(dt_bias), _f64(z), _f64(h0)
     pos = np.ascontiguousarray(pos, dtype=np.int32)
@@ -299,13 +300,14 @@ def scan_fwd_ext(u, dt, A, B, C, D, dt_bias, pos, z=None, h0=None, softplus=True
     out = np.empty_like(u)
     h_last = np.empty((R, Dn, N))
     lib().pmo_scan_fwd_ext(_p(u), _p(dt), _p(A), _p(B), _p(C), _p(D), _p(dt_bias),
-                           int(bool(softplus)), _p(pos, _i32p), _p(z), _p(h0), _p(out),
+                           int(bool(softplus)), int(bool(zoh)), _p(pos, _i32p), _p(z), _p(h0),
+                           _p(out),
                            _p(h_last), R, Dn, L, N)
     return out, h_last
 
 
 def scan_bwd_ext(u, dt, A, B, C, D, dt_bias, pos, dout, z=None, h0=None, dh_last=None,
-                 softplus=True):
+                 softplus=True, zoh=False):
     """Adjoint of scan_fwd_ext -> dict(du, ddt, dA, dB, dC, dD, ddt_bias, dz, dh0)."""
     u, dt, A, B, C = _f64(u), _f64(dt), _f64(A), _f64(B), _f64(C)
     D, dt_bias, z, h0 = _f64(D), _f64(dt_bias), _f64(z), _f64(h0)
@@ -318,7 +320,8 @@ def scan_bwd_ext(u, dt, A, B, C, D, dt_bias, pos, dout, z=None, h0=None, dh_last
              ddt_bias=np.empty(Dn), dz=np.zeros_like(u) if z is not None else None,
              dh0=np.zeros((R, Dn, N)) if h0 is not None else None)
     lib().pmo_scan_bwd_ext(_p(u), _p(dt), _p(A), _p(B), _p(C), _p(D), _p(dt_bias),
-                           int(bool(softplus)), _p(pos, _i32p), _p(z), _p(h0), _p(dout),
+                           int(bool(softplus)), int(bool(zoh)), _p(pos, _i32p), _p(z), _p(h0),
+                           _p(dout),
                            _p(dh_last), _p(o["du"]), _p(o["ddt"]), _p(o["dA"]), _p(o["dB"]),
                            _p(o["dC"]), _p(o["dD"]), _p(o["ddt_bias"]), _p(o["dz"]),
                            _p(o["dh0"]), R, Dn, L, N)

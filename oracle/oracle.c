@@ -553,9 +553,20 @@ static int is_head_ext(const int32_t* pos_row, int64_t t, const double* h0) {
     return pos_row[t] == 0 || (t == 0 && h0 == NULL);
 }
 
+/* Eq 2b: f(z) = (e^z - 1)/z, the factor with bbar = f(delta A) delta B;
+ * Taylor 1 + z/2 + z^2/6 below |z| = 1e-4. */
+static double zoh_f(double z) {
+    return fabs(z) < 1e-4 ? 1.0 + z / 2.0 + z * z / 6.0 : expm1(z) / z;
+}
+/* f'(z) = (e^z - f(z)) / z = (z e^z - e^z + 1) / z^2; Taylor below 1e-3 */
+static double zoh_df(double z) {
+    return fabs(z) < 1e-3 ? 0.5 + z / 3.0 + z * z / 8.0 + z * z * z / 30.0
+                          : (exp(z) - zoh_f(z)) / z;
+}
+
 void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
                       const double* B, const double* C, const double* D,
-                      const double* dt_bias, int32_t softplus,
+                      const double* dt_bias, int32_t softplus, int32_t zoh,
                       const int32_t* pos, const double* z, const double* h0,
                       double* out, double* h_last,
                       int64_t R, int64_t Dn, int64_t L, int32_t N) {
@@ -573,7 +584,9 @@ void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
                 double yt = 0.0;
                 const int head = is_head_ext(pos + r * L, t, h0);
                 for (int32_t n = 0; n < N; ++n) {
-                    double bx = delta * B[(r * N + n) * L + t] * x;
+                    /* Euler (Q1): bbar = delta B;  ZOH (Eq 2b): bbar = f(delta A) delta B */
+                    double bfac = zoh ? zoh_f(delta * A[d * N + n]) * delta : delta;
+                    double bx = bfac * B[(r * N + n) * L + t] * x;
                     h[n] = head ? bx : exp(delta * A[d * N + n]) * h[n] + bx;
                     yt += C[(r * N + n) * L + t] * h[n];
                 }
@@ -595,7 +608,7 @@ void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
  * Param grads (dA, dD, ddt_bias) and dB, dC are overwritten sums. */
 void pmo_scan_bwd_ext(const double* u, const double* dt, const double* A,
                       const double* B, const double* C, const double* D,
-                      const double* dt_bias, int32_t softplus,
+                      const double* dt_bias, int32_t softplus, int32_t zoh,
                       const int32_t* pos, const double* z, const double* h0,
                       const double* dout, const double* dh_last,
                       double* du, double* ddt, double* dA, double* dB,
@@ -634,7 +647,8 @@ void pmo_scan_bwd_ext(const double* u, const double* dt, const double* A,
                 const int head = is_head_ext(pr, t, h0);
                 for (int32_t n = 0; n < N; ++n) {
                     double abar = head ? 0.0 : exp(delta * A[d * N + n]);
-                    double bx = delta * B[(r * N + n) * L + t] * u[lane + t];
+                    double bfac = zoh ? zoh_f(delta * A[d * N + n]) * delta : delta;
+                    double bx = bfac * B[(r * N + n) * L + t] * u[lane + t];
                     hs[(t + 1) * N + n] = head ? bx : abar * hs[t * N + n] + bx;
                     as[t * N + n] = abar;
                 }
@@ -654,19 +668,29 @@ void pmo_scan_bwd_ext(const double* u, const double* dt, const double* A,
                     dz[lane + t] = gy * yt * s * (1.0 + zz * (1.0 - s));
                     gy = gy * zz * s;
                 }
-                double S = 0.0, dq = 0.0;
+                /* du = D gy + sum_n g B bfac (Euler: delta * sum_n g B);
+                 * Sd = sum_n g B d(bfac)/d(delta) */
+                double Sb = 0.0, Sd = 0.0, dq = 0.0;
                 for (int32_t n = 0; n < N; ++n) {
+                    const double Bn = B[(r * N + n) * L + t];
+                    const double zn = delta * A[d * N + n];
+                    /* bfac = delta (Euler) or f(z) delta = (e^z - 1)/A (ZOH):
+                     * d bfac/d delta = 1 or e^z;  d bfac/dA = 0 or delta^2 f'(z) */
+                    const double bfac = zoh ? zoh_f(zn) * delta : delta;
+                    const double dbdd = zoh ? exp(zn) : 1.0;
                     g[n] = C[(r * N + n) * L + t] * gy + carry[n];
-                    S += g[n] * B[(r * N + n) * L + t];
+                    Sb += zoh ? g[n] * Bn * bfac : g[n] * Bn;
+                    Sd += g[n] * Bn * dbdd;
                     double q = g[n] * as[t * N + n] * hs[t * N + n];
                     dq += A[d * N + n] * q;
                     dA[d * N + n] += delta * q;
-                    myB[n * L + t] += g[n] * delta * x;
+                    if (zoh) dA[d * N + n] += g[n] * Bn * x * delta * delta * zoh_df(zn);
+                    myB[n * L + t] += g[n] * bfac * x;
                     myC[n * L + t] += gy * hs[(t + 1) * N + n];
                     carry[n] = as[t * N + n] * g[n];
                 }
-                du[lane + t] = (D ? D[d] : 0.0) * gy + delta * S;
-                double gd = (x * S + dq) * (softplus ? sigmoid_d(v) : 1.0);
+                du[lane + t] = (D ? D[d] : 0.0) * gy + (zoh ? Sb : delta * Sb);
+                double gd = (x * Sd + dq) * (softplus ? sigmoid_d(v) : 1.0);
                 ddt[lane + t] = gd;
                 if (dD) dD[d] += gy * x;
                 if (ddt_bias) ddt_bias[d] += gd;

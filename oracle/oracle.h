@@ -118,7 +118,11 @@ void pmo_seq_scan_bwd(const double* u, const double* dt, const double* A,
                       double* dB, double* dC, double* dD, double* ddt_bias,
                       int64_t Dn, int64_t Ls, int32_t N);
 
-/* ---- NEXT-1 / NEXT-2: gate z, state passing h0 / h_last ------------------ */
+/* ---- NEXT-1 / NEXT-2: gate z, state passing h0 / h_last; NEXT-4: ZOH ----- */
+/* zoh != 0 selects Eq 2b for B-bar instead of the Euler reading Q1:
+ *   bbar = f(z) * delta * B,  z = delta * A[d,n],  f(z) = (e^z - 1) / z,
+ * with f(z) = 1 + z/2 + z^2/6 for |z| < 1e-4 (removable
+ * singularity); f is evaluated with expm1 elsewhere.                       */
 /* out = y * silu(z) if z != NULL (else y); h0 (R,Dn,N): state entering t=0
  * of a row whose slot 0 is not a sequence start (P:275 future work);
  * head(r,t) := pos[r,t]==0 || (t==0 && h0==NULL).  h_last (R,Dn,N): state
@@ -126,13 +130,13 @@ void pmo_seq_scan_bwd(const double* u, const double* dt, const double* A,
  * h_last; outputs dz (if z) and dh0 (if h0) in addition.                    */
 void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
                       const double* B, const double* C, const double* D,
-                      const double* dt_bias, int32_t softplus,
+                      const double* dt_bias, int32_t softplus, int32_t zoh,
                       const int32_t* pos, const double* z, const double* h0,
                       double* out, double* h_last,
                       int64_t R, int64_t Dn, int64_t L, int32_t N);
 void pmo_scan_bwd_ext(const double* u, const double* dt, const double* A,
                       const double* B, const double* C, const double* D,
-                      const double* dt_bias, int32_t softplus,
+                      const double* dt_bias, int32_t softplus, int32_t zoh,
                       const int32_t* pos, const double* z, const double* h0,
                       const double* dout, const double* dh_last,
                       double* du, double* ddt, double* dA, double* dB,
