@@ -224,6 +224,12 @@ PM_API pm_status pm_selective_scan_bwd(const void* u, const void* dt,
  *    state between the parts", the paper's future work)
  * ===========================================================================
  * Same recurrence as pm_selective_scan_fwd, with:
+ *   zoh: 0 = Euler B-bar = delta*B (north_star, reading
+ *     Q1); 1 = zero-order hold, Eq 2b:
+ *       B-bar = f(z)*delta*B,  z = delta*A[d,n],  f(z) = (e^z - 1)/z
+ *     (f evaluated as (abar - 1)/A for |z| >= 0.1 and by its Taylor series
+ *     below, so f(0) = 1 and A = 0 is allowed).  The reset still selects
+ *     h = B-bar*u at heads.
  *   z (optional, (R,Dn,L) io dtype):  out[r,d,t] = y[r,d,t] * silu(z[r,d,t]),
  *     silu(z) = z / (1 + exp(-z)); with z == NULL, out = y.
  *   h0 (optional, (R,Dn,N) fp32): the state entering slot 0 of each row.
@@ -238,13 +244,14 @@ PM_API pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt,
                                    const float* A, const void* B,
                                    const void* C, const float* Dskip,
                                    const float* dt_bias, int32_t dt_softplus,
-                                   const int32_t* pos, const void* z,
-                                   const float* h0, void* out, float* states,
+                                   int32_t zoh, const int32_t* pos,
+                                   const void* z, const float* h0, void* out,
+                                   float* states,
                                    float* h_last, int64_t R, int64_t Dn,
                                    int64_t L, int32_t N, pm_dtype io,
                                    pm_stream_t stream);
 
-/* Backward of pm_selective_scan_fwd_ex, given dout = dLoss/d(out) and
+/* Backward of pm_selective_scan_fwd_ex (same zoh), given dout = dLoss/d(out) and
  * dh_last = dLoss/d(h_last) (optional, (R,Dn,N) fp32; NULL = 0):
  *   dy  = dout * silu(z)                (dy = dout when z == NULL)
  *   dz  = dout * y * silu'(z),  silu'(z) = s (1 + z (1 - s)), s = sigmoid(z)
@@ -259,8 +266,9 @@ PM_API pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt,
                                    const float* A, const void* B,
                                    const void* C, const float* Dskip,
                                    const float* dt_bias, int32_t dt_softplus,
-                                   const int32_t* pos, const void* z,
-                                   const float* h0, const float* states,
+                                   int32_t zoh, const int32_t* pos,
+                                   const void* z, const float* h0,
+                                   const float* states,
                                    const void* dout, const float* dh_last,
                                    void* du, void* ddt, float* dA, float* dB,
                                    float* dC, float* dD, float* ddt_bias,

@@ -80,9 +80,9 @@ def lib():
         L.pm_selective_scan_bwd_workspace.argtypes = [_i64, _i64, _i64, _i32, _i32]
         L.pm_selective_scan_bwd.argtypes = ([_vp] * 7 + [_i32] + [_vp] * 10 + [_vp, _sz] +
                                             [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
-        L.pm_selective_scan_fwd_ex.argtypes = ([_vp] * 7 + [_i32] + [_vp] * 6 +
+        L.pm_selective_scan_fwd_ex.argtypes = ([_vp] * 7 + [_i32, _i32] + [_vp] * 6 +
                                                [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
-        L.pm_selective_scan_bwd_ex.argtypes = ([_vp] * 7 + [_i32] + [_vp] * 15 + [_vp, _sz] +
+        L.pm_selective_scan_bwd_ex.argtypes = ([_vp] * 7 + [_i32, _i32] + [_vp] * 15 + [_vp, _sz] +
                                                [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
         for f in EXPORTED_SYMBOLS:
             if f not in ("pm_status_string", "pm_version") and not f.endswith(
@@ -313,10 +313,11 @@ def pm_selective_scan_bwd(u, dt, A, B, C, Dskip, dt_bias, pos, dy, states=None,
 
 def pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, z=None, h0=None, out=None,
                              states=None, h_last=None, dt_softplus=True, want_states=True,
-                             want_last_state=False):
+                             want_last_state=False, zoh=False):
     """Extended ScanOp_pack forward: fused gate ``out = y * silu(z)`` (SURVEY
     NEXT-1) and cross-row state passing ``h0 -> h_last`` (NEXT-2, the
-    paper's future work P:275).  Returns (out, states, h_last)."""
+    paper's future work P:275); ``zoh`` selects Eq 2b's B-bar (NEXT-4)
+    instead of Euler.  Returns (out, states, h_last)."""
     import torch
     _dev(u, dt, A, B, C, Dskip, dt_bias, pos, z, h0)
     R, Dn, L = u.shape
@@ -330,14 +331,15 @@ def pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, z=None, h0=Non
     _dev(out, states, h_last)
     _check(lib().pm_selective_scan_fwd_ex(
         _ptr(u), _ptr(dt), _ptr(A), _ptr(B), _ptr(C), _ptr(Dskip), _ptr(dt_bias),
-        int(bool(dt_softplus)), _ptr(pos), _ptr(z), _ptr(h0), _ptr(out), _ptr(states),
+        int(bool(dt_softplus)), int(bool(zoh)), _ptr(pos), _ptr(z), _ptr(h0), _ptr(out),
+        _ptr(states),
         _ptr(h_last), R, Dn, L, N, _io(u), _stream(u)), "pm_selective_scan_fwd_ex")
     return out, states, h_last
 
 
 def pm_selective_scan_bwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, dout, z=None, h0=None,
                              states=None, dh_last=None, dt_softplus=True, out=None,
-                             workspace=None, want_dh0=None):
+                             workspace=None, want_dh0=None, zoh=False):
     """Adjoint of pm_selective_scan_fwd_ex.  Returns dict du, ddt, dA, dB, dC,
     dD, ddt_bias, dz (when z is given), dh0 (when h0 is given or want_dh0)."""
     import torch
@@ -364,7 +366,8 @@ def pm_selective_scan_bwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, dout, z=None, 
     _dev(workspace, *[v for v in o.values() if v is not None])
     _check(lib().pm_selective_scan_bwd_ex(
         _ptr(u), _ptr(dt), _ptr(A), _ptr(B), _ptr(C), _ptr(Dskip), _ptr(dt_bias),
-        int(bool(dt_softplus)), _ptr(pos), _ptr(z), _ptr(h0), _ptr(states), _ptr(dout),
+        int(bool(dt_softplus)), int(bool(zoh)), _ptr(pos), _ptr(z), _ptr(h0), _ptr(states),
+        _ptr(dout),
         _ptr(dh_last), _ptr(o["du"]), _ptr(o["ddt"]), _ptr(o["dA"]), _ptr(o["dB"]),
         _ptr(o["dC"]), _ptr(o["dD"]), _ptr(o["ddt_bias"]), _ptr(o["dz"]), _ptr(o["dh0"]),
         _ptr(workspace), workspace.numel(), R, Dn, L, N, _io(u), _stream(u)),

@@ -28,6 +28,32 @@ PM_DEV float rcp(float x) {  // MUFU.RCP
 }
 PM_DEV float sigmoidf_fast(float v) { return rcp(1.f + ex2(-v * kLog2e)); }
 
+// Eq 2b (ZOH): B-bar = f(z) delta B, f(z) = (e^z - 1)/z, z = delta A.
+// bfac = f(z) delta: for |z| >= 0.1 as (abar - 1) / A from the abar = e^z the
+// scan computes anyway; below, delta (1 + z/2 + z^2/6 + z^3/24 + z^4/120)
+// (truncation < 2e-8 relative; no cancellation).  A select, so A = 0 (1/A =
+// inf) takes the series.  dfp = delta f'(z) = (e^z - f)/A, series
+// delta (1/2 + z/3 + z^2/8 + z^3/30 + z^4/144).
+PM_DEV float zoh_series_f(float z) {
+  return fmaf(z, fmaf(z, fmaf(z, fmaf(z, 1.f / 120.f, 1.f / 24.f), 1.f / 6.f), 0.5f), 1.f);
+}
+PM_DEV float zoh_series_df(float z) {
+  return fmaf(z, fmaf(z, fmaf(z, fmaf(z, 1.f / 144.f, 1.f / 30.f), 1.f / 8.f), 1.f / 3.f), 0.5f);
+}
+PM_DEV float zoh_bfac(float ab, float z, float invA, float dl) {
+  return fabsf(z) < 0.1f ? dl * zoh_series_f(z) : fmaf(ab, invA, -invA);
+}
+// (bfac, delta f'(z)); rdl = 1/delta
+PM_DEV void zoh_coef(float ab, float z, float invA, float dl, float rdl, float& bfac, float& dfp) {
+  if (fabsf(z) < 0.1f) {
+    bfac = dl * zoh_series_f(z);
+    dfp = dl * zoh_series_df(z);
+  } else {
+    bfac = fmaf(ab, invA, -invA);
+    dfp = fmaf(-bfac, rdl, ab) * invA;
+  }
+}
+
 // Packed fp32x2 arithmetic (sm_100a FFMA2/FMUL2/FADD2): two IEEE fp32
 // operations per instruction, bit-identical to the scalar ones.
 PM_DEV float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }

@@ -1,1065 +1,11 @@
-// scan.cu -- ScanOp_pack forward/backward for sm_100a (Alg 2 P:172-185,
-// Eq 1a/1b/2a P:202-205, sec 3.4 P:199-224 of arXiv 2408.03865).
-//
-// Design:
-//  * one thread = one (row, channel) lane holding all N states in registers,
-//    sequential in time; a CTA = 128 consecutive channels of one row, so the
-//    head predicate is CTA-uniform (no divergence) and B/C/pos tiles are
-//    staged once in shared memory (fp32) and broadcast to all channels;
-//  * time parallelism comes from the packing itself: a row is split at
-//    sequence heads into independent segments (sequences never span
-//    rows, and the reset cuts every carry), so no carry fix-up and no
-//    redundant exponentials are needed;
-//  * the reset is a select on the CTA-uniform head flag (h = b), never a
-//    multiply by 0, so NaN/Inf and -0 cannot cross a boundary;
-//  * forward saves the state every kChunk steps ("reused Mamba's structure
-//    for handling hidden_state"); backward walks chunks in reverse,
-//    recomputes kSub-step sub-chunks into registers, runs the reverse
-//    recurrence g_t = C_t dy_t + abar_{t+1} g_{t+1} (abar = 0 at heads,
-//    P:224) and reduces dB/dC over channels with a warp transpose through
-//    shared memory, then over warps, into per-channel-block partials that a
-//    finalize kernel sums in a fixed order (deterministic).
-#include <algorithm>
-#include <cstdlib>
-#include <cstdio>
-#include <type_traits>
+// scan.cu -- C ABI of ScanOp_pack (include/pm.h): argument validation,
+// workspace / states layout, dispatch to the kernels in scan_fwd.cu and
+// scan_bwd.cu.
+#include "scan_impl.cuh"
 
-#include "common.cuh"
-
-namespace pm {
-
-constexpr int kScanThreads = 128;
-constexpr int kScanWarps = kScanThreads / 32;
-constexpr int kTile = 64;   // fwd staging tile (time steps)
-constexpr int kChunk = 16;  // checkpoint interval (time steps)
-constexpr int kSub = 4;     // bwd register sub-chunk (time steps)
-constexpr int kNSub = kChunk / kSub;
-constexpr int kFwdMinB = 4;  // resident fwd CTAs per SM (register cap 128)
-constexpr int kBwdMinB = 4;  // resident bwd CTAs per SM (register cap 128; smem fits 4)
-
-struct ScanFwdArgs {
-  const void* u;
-  const void* dt;
-  const float* A;
-  const void* B;
-  const void* C;
-  const float* Dskip;
-  const float* dt_bias;
-  const int32_t* pos;
-  void* y;
-  float* states;
-  const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
-  int* counter;       // work counter for the persistent loop
-  int n_items;
-  int R, Dn, L, nseg, nchunk, softplus;
-  const void* z;      // NEXT-1 gate (R,Dn,L) or NULL: y <- y * silu(z)
-  const float* h0;    // NEXT-2 state entering t=0 (R,Dn,N) or NULL
-  float* h_last;      // state after step L-1 (R,Dn,N) or NULL
-};
-
-struct ScanBwdArgs {
-  const void* u;
-  const void* dt;
-  const float* A;
-  const void* B;
-  const void* C;
-  const float* Dskip;
-  const float* dt_bias;
-  const int32_t* pos;
-  const float* states;
-  const void* dy;
-  void* du;
-  void* ddt;
-  float* ws_bc;     // (nDblk, R, L, 2N)
-  float* ws_param;  // (R*nseg, N+2, Dn)
-  const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
-  int* counter;
-  int n_items;
-  int R, Dn, L, nseg, nchunk, softplus;
-  const void* z;        // NEXT-1 gate (R,Dn,L) or NULL; dy is then d(out)
-  const float* h0;      // NEXT-2 state entering t=0 (R,Dn,N) or NULL
-  const float* dh_last; // cotangent of the state after step L-1 or NULL
-  void* dz;             // (R,Dn,L) when z != NULL
-  float* dh0;           // (R,Dn,N) when h0 != NULL
-};
-
-// ---------------------------------------------------------------------------
-// Work scheduling.  Segment lengths follow the sequence-length distribution
-// (57..2048 steps), so a plain grid leaves a long tail.  A planning kernel
-// lists every row's segments, one CTA sorts them longest-first, and the scan
-// kernels are persistent: each CTA pulls (segment, channel-block) items from
-// an atomic counter in that order (LPT), so the last items are the shortest.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) seg_plan_kernel(const int32_t* __restrict__ pos, int L,
-                                                      int nseg, int4* __restrict__ items) {
-  // cut k (1 <= k < nseg) = first head at or after k * ceil(L / nseg), as in
-  // segment_bounds(); one warp per cut, 32 positions per ballot
-  __shared__ int cut[65];
-  const int r = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t* pos_row = pos + (int64_t)r * L;
-  const int seg = (L + nseg - 1) / nseg;
-  for (int k = 1 + warp; k < nseg; k += blockDim.x >> 5) {
-    int b = L;
-    for (int base = k * seg; base < L; base += 32) {
-      const int t = base + lane;
-      const unsigned m = __ballot_sync(0xffffffffu, t < L && __ldg(pos_row + t) == 0);
-      if (m) {
-        b = base + __ffs(m) - 1;
-        break;
-      }
-    }
-    if (lane == 0) cut[k] = min(b, L);
-  }
-  if (threadIdx.x == 0) {
-    cut[0] = 0;
-    cut[nseg] = L;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < nseg; k += blockDim.x)
-    items[r * nseg + k] = make_int4(r, k, cut[k], max(cut[k], cut[k + 1]));
-}
-
-// Longest-first order of the segment list (one CTA).  n <= 4096: exact rank
-// sort (length descending, ties by index); larger n: bucket sort on 1024
-// length bins (order within a bin is arbitrary -- results never depend on
-// the processing order, only the load balance does).
-__global__ void __launch_bounds__(1024) seg_sort_kernel(const int4* __restrict__ in, int n, int L,
-                                                       int4* __restrict__ out) {
-  if (n <= 4096) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const int4 a = in[i];
-      const int la = a.w - a.z;
-      int rank = 0;
-      for (int j = 0; j < n; ++j) {
-        const int4 b = in[j];
-        const int lb = b.w - b.z;
-        rank += (lb > la) || (lb == la && j < i);
-      }
-      out[rank] = a;
-    }
-    return;
-  }
-  constexpr int kBins = 1024;
-  __shared__ int cnt[kBins];
-  for (int b = threadIdx.x; b < kBins; b += blockDim.x) cnt[b] = 0;
-  __syncthreads();
-  auto bin_of = [&](const int4 v) {  // longest first: bin 0 = longest
-    const int len = v.w - v.z;
-    return kBins - 1 - (int)(((int64_t)len * (kBins - 1)) / max(L, 1));
-  };
-  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[bin_of(in[i])], 1);
-  __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive scan -> bin cursors
-    int acc = 0;
-    for (int b = 0; b < kBins; ++b) {
-      const int c = cnt[b];
-      cnt[b] = acc;
-      acc += c;
-    }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const int4 v = in[i];
-    out[atomicAdd(&cnt[bin_of(v)], 1)] = v;
-  }
-}
-
-// next work item: persistent (sorted list + counter) or grid mode (1 item)
-struct Work {
-  int r, k, dblk, s0, s1;
-  bool valid;
-};
-
-// Stage B, C (converted to fp32, time-major [t][n]) and head flags for the
-// time window [j0, j0 + W) of row r into shared memory.
-template <typename T, int N, int W, bool kVec>
-PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
-                     const int32_t* __restrict__ pos_row, int L, int j0,
-                     float (*sB)[N], float (*sC)[N], unsigned* sMask, bool t0_head) {
-  static_assert(W % 8 == 0, "window must be a multiple of 8");
-  for (int e = threadIdx.x; e < N * (W / 8); e += blockDim.x) {
-    const int n = e % N, tb = (e / N) * 8;
-    float vb[8], vc[8];
-    load8<T, kVec>(B_r + (int64_t)n * L, j0 + tb, L, vb);
-    load8<T, kVec>(C_r + (int64_t)n * L, j0 + tb, L, vc);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      sB[tb + i][n] = vb[i];
-      sC[tb + i][n] = vc[i];
-    }
-  }
-  // head flags of the window as a bitmask (warp 0 ballots 32 steps at a time)
-  if (threadIdx.x < 32) {
-#pragma unroll
-    for (int w0 = 0; w0 < W; w0 += 32) {
-      const int t = j0 + w0 + (int)threadIdx.x;
-      const bool f = (w0 + (int)threadIdx.x < W) &&
-                     ((t >= L) || (t == 0 && t0_head) || __ldg(pos_row + t) == 0);
-      const unsigned m = __ballot_sync(0xffffffffu, f);
-      if (threadIdx.x == 0) sMask[w0 / 32] = m;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// forward
-// ---------------------------------------------------------------------------
-template <typename T, int N, bool kVec, int MinB, bool kGate>
-__global__ void __launch_bounds__(kScanThreads, MinB)
-scan_fwd_kernel(const ScanFwdArgs a) {
-  __shared__ __align__(16) float sB[kTile][N];
-  __shared__ __align__(16) float sC[kTile][N];
-  __shared__ unsigned sMask[kTile / 32];
-  __shared__ int s_red[kScanWarps];
-  __shared__ int s_work;
-
-  const int L = a.L, Dn = a.Dn;
-  const int ndblk = (Dn + kScanThreads - 1) / kScanThreads;
-  for (int iter = 0;; ++iter) {
-  int r, dblk, s0, s1;
-  if (a.items != nullptr) {  // persistent: longest segments first
-    __syncthreads();
-    if (threadIdx.x == 0) s_work = atomicAdd(a.counter, 1);
-    __syncthreads();
-    const int w = s_work;
-    if (w >= a.n_items * ndblk) break;
-    const int4 it = a.items[w / ndblk];
-    r = it.x;
-    dblk = w % ndblk;
-    s0 = it.z;
-    s1 = it.w;
-  } else {
-    if (iter > 0) break;
-    r = blockIdx.y;
-    dblk = blockIdx.x;
-    segment_bounds(a.pos + (int64_t)r * L, L, blockIdx.z, a.nseg, s_red, s0, s1);
-  }
-  if (s0 >= s1) continue;
-  const int d_raw = dblk * kScanThreads + threadIdx.x;
-  const bool active = d_raw < Dn;
-  const int d = active ? d_raw : Dn - 1;
-  const int32_t* pos_row = a.pos + (int64_t)r * L;
-
-  const T* B_r = static_cast<const T*>(a.B) + (int64_t)r * N * L;
-  const T* C_r = static_cast<const T*>(a.C) + (int64_t)r * N * L;
-  const int64_t lane = ((int64_t)r * Dn + d) * L;
-  const T* u_row = static_cast<const T*>(a.u) + lane;
-  const T* dt_row = static_cast<const T*>(a.dt) + lane;
-  T* y_row = a.y ? static_cast<T*>(a.y) + lane : nullptr;
-  const T* z_row = kGate ? static_cast<const T*>(a.z) + lane : nullptr;
-
-  // states are processed in pairs with packed fp32x2 arithmetic (FFMA2)
-  constexpr int NP = N / 2;
-  float2 A2[NP];
-#pragma unroll
-  for (int p = 0; p < NP; ++p)
-    A2[p] = make_float2(__ldg(a.A + (int64_t)d * N + 2 * p) * kLog2e,
-                        __ldg(a.A + (int64_t)d * N + 2 * p + 1) * kLog2e);
-  const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
-  const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
-
-  float2 h[NP];
-#pragma unroll
-  for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
-  if (s0 == 0 && a.h0 != nullptr) {  // NEXT-2: state carried into the row
-    const float* hp = a.h0 + ((int64_t)r * Dn + d) * N;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) h[p] = make_float2(__ldg(hp + 2 * p), __ldg(hp + 2 * p + 1));
-  }
-
-  // Flat loop over 8-step sub-blocks; u/dt of the next sub-block are loaded
-  // into registers before the current one is computed (software pipeline),
-  // B/C/head tiles are restaged at every kTile boundary.  Sub-blocks fully
-  // inside the segment (all but at most two) run without per-step checks.
-  int tb = s0 & ~7;
-  Raw8<T, kVec> pu, pt, pz;
-  pu.load(u_row, tb, L);
-  pt.load(dt_row, tb, L);
-  if (kGate) pz.load(z_row, tb, L);
-  int j0 = -1;
-  unsigned long long hmask = 0ull;
-  for (; tb < s1; tb += 8) {
-    if (j0 < 0 || (tb & (kTile - 1)) == 0) {  // CTA-uniform
-      j0 = tb & ~(kTile - 1);
-      __syncthreads();
-      stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask, a.h0 == nullptr);
-      __syncthreads();
-      // head flags of the tile as a register bitmask (CTA-uniform): no
-      // shared-memory load on the per-step critical path
-      hmask = (unsigned long long)sMask[0] | ((unsigned long long)sMask[1] << 32);
-    }
-    float uu[8], vv[8], yy[8], zz[8];
-    pu.unpack(uu);
-    pt.unpack(vv);
-    if (kGate) pz.unpack(zz);
-    if (tb + 8 < s1) {
-      pu.load(u_row, tb + 8, L);
-      pt.load(dt_row, tb + 8, L);
-      if (kGate) pz.load(z_row, tb + 8, L);
-    }
-    const int sb = tb - j0;
-    // checkpoint = state before step tb (only step i == 0 can be a multiple of kChunk)
-    if (a.states != nullptr && (tb % kChunk) == 0 && tb >= s0 && active) {
-      float* st = a.states + (((int64_t)r * a.nchunk + tb / kChunk) * N) * Dn + d;
-#pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        st[(int64_t)(2 * p) * Dn] = h[p].x;
-        st[(int64_t)(2 * p + 1) * Dn] = h[p].y;
-      }
-    }
-    auto block = [&](auto full_tag) {
-      constexpr bool kFull = decltype(full_tag)::value;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int t = tb + i;
-        yy[i] = 0.f;
-        if (!kFull && (t < s0 || t >= s1)) continue;  // CTA-uniform
-        const float v = vv[i] + bias;
-        const float delta = a.softplus ? softplusf(v) : v;
-        const float2 dux2 = f2(delta * uu[i]), dl2 = f2(delta);
-        const float2* Bt = reinterpret_cast<const float2*>(sB[sb + i]);
-        const float2* Ct = reinterpret_cast<const float2*>(sC[sb + i]);
-        if ((hmask >> (sb + i)) & 1ull) {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
-        } else {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) h[p] = ffma2(ex2x2(fmul2(dl2, A2[p])), h[p], fmul2(dux2, Bt[p]));
-        }
-        float2 yp[2] = {make_float2(Dd * uu[i], 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int p = 0; p < NP; ++p) yp[p & 1] = ffma2(Ct[p], h[p], yp[p & 1]);
-        const float2 ys = fadd2(yp[0], yp[1]);
-        yy[i] = ys.x + ys.y;
-        if (kGate) yy[i] *= zz[i] * sigmoidf_fast(zz[i]);  // out = y * silu(z)
-      }
-    };
-    if (tb >= s0 && tb + 8 <= s1) block(std::true_type{});
-    else block(std::false_type{});
-    if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
-  }
-  if (s1 == L && a.h_last != nullptr && active) {  // state after the row's last step
-    float* hp = a.h_last + ((int64_t)r * Dn + d) * N;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      hp[2 * p] = h[p].x;
-      hp[2 * p + 1] = h[p].y;
-    }
-  }
-  }  // work loop
-}
-
-// ---------------------------------------------------------------------------
-// backward
-// ---------------------------------------------------------------------------
-// Layout: a CTA owns kBwdCh channels of one row and one time segment; each
-// channel is served by a lane pair (lane = 2*c + hf), thread hf holding the
-// NH = N/2 states [hf*NH, hf*NH + NH) -- half the registers of a
-// one-thread-per-channel design, so 12 warps fit per SM.
-// Per chunk of kChunk steps (walked in reverse):
-//   staging: every per-chunk input (u, dt, dy rows, B, C, pos, the saved
-//            chunk state) is fetched with cp.async one chunk AHEAD into a raw
-//            shared buffer, so no global latency sits on the critical path;
-//   phase 1: per-(t,d) scalars delta, u, dy, softplus'(v) computed once into
-//            shared memory; B/C converted to fp32; head flags;
-//   pass A : forward recompute from the saved chunk state, storing the state
-//            at every kSub-step sub-chunk start (shared memory);
-//   pass B : per sub-chunk (reverse): recompute h_t, abar_t into registers,
-//            then the reverse recurrence g_t = C_t dy_t + abar_{t+1} g_{t+1}
-//            (abar = 0 at heads); sum_n terms are combined across the
-//            lane pair with one shuffle; dB/dC values are reduced over each
-//            warp's channels in 2-step rounds (warp transpose through a
-//            conflict-free padded buffer) and the per-warp partials of the
-//            whole chunk are summed across warps after ONE barrier.
-constexpr int kBwdCh = 64;                   // channels per CTA
-constexpr int kBwdThreads = 2 * kBwdCh;      // lane pair per channel
-constexpr int kBwdWarps = kBwdThreads / 32;
-constexpr int kRedStride = 32;               // float4 per transpose row (no padding)
-constexpr int kBSub = 2;                     // bwd register sub-chunk (= one reduction round)
-constexpr int kBNSub = kChunk / kBSub;
-static_assert(kChunk == 16, "phase 1 maps 8 steps to each thread of a pair");
-
-template <typename T, int N, bool kGate>
-struct BwdRaw {  // raw inputs of one chunk, filled by cp.async (vector path)
-  T u[kBwdCh][kChunk];
-  T dt[kBwdCh][kChunk];
-  T dy[kBwdCh][kChunk];
-  T z[kGate ? kBwdCh : 1][kChunk];
-  T B[N][kChunk];
-  T C[N][kChunk];
-  int32_t pos[kChunk];
-  float st[N][kBwdCh];
-};
-
-template <typename T, int N, bool kGate>
-struct BwdSmem {
-  static constexpr int NH = N / 2;   // states per thread
-  static constexpr int kQ = N / 4;   // float4 quads of (dB, dC) values per thread-step
-  static constexpr int kRows = 2 * kQ;  // transpose rows per 2-step round
-  BwdRaw<T, N, kGate> raw;
-  float4 sc[kChunk][kBwdCh];  // per-(t,d) scalars {delta, u, dy, softplus'(v)}
-                              // (u = dy = 0 on inactive channels; with the
-                              // gate, dy = dout * silu(z))
-  float sgz[kGate ? kChunk : 1][kBwdCh];  // dout * silu'(z) (gate only)
-  float4 red[kBwdWarps][kRows][kRedStride];
-  float4 xw[kChunk / 2][kBwdWarps][kRows][2];
-  float B[kChunk][N];
-  float C[kChunk][N];
-  unsigned hmask[1];  // head flags of the chunk (bit e = step cb + e)
-  int s_red[kBwdWarps];
-  uint32_t tmem_base;
-};
-
-// Issue the cp.async copies of chunk c's raw inputs (vector path only:
-// L*isz % 16 == 0, Dn % 4 == 0, 16-byte aligned pointers).
-template <typename T, int N, bool kGate>
-PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, int dblk, int c,
-                          int s0) {
-  constexpr int kEl = 16 / (int)sizeof(T);       // elements per 16-byte chunk
-  constexpr int kRowQ = kChunk / kEl;            // chunks per (row, chunk)
-  const int L = a.L, Dn = a.Dn, cb = c * kChunk;
-  constexpr int kTx = kBwdCh * kRowQ;
-#pragma unroll
-  for (int arr = 0; arr < (kGate ? 4 : 3); ++arr) {  // u, dt, dy (, z)
-    const T* base = static_cast<const T*>(arr == 0 ? a.u : arr == 1 ? a.dt : arr == 2 ? a.dy : a.z);
-    T(*dst)[kChunk] = arr == 0 ? rw.u : arr == 1 ? rw.dt : arr == 2 ? rw.dy : rw.z;
-    for (int e = threadIdx.x; e < kTx; e += kBwdThreads) {
-      const int ch = e / kRowQ, q = e % kRowQ;
-      const int d = dblk * kBwdCh + ch;
-      const int t0 = cb + q * kEl;
-      const bool ok = d < Dn && t0 < L;
-      const T* src = ok ? base + ((int64_t)r * Dn + d) * L + t0 : base;
-      cp_async16(&dst[ch][q * kEl], src, ok ? 16 : 0);
-    }
-  }
-  const T* Bp = static_cast<const T*>(a.B) + (int64_t)r * N * L;
-  const T* Cp = static_cast<const T*>(a.C) + (int64_t)r * N * L;
-  for (int e = threadIdx.x; e < 2 * N * kRowQ; e += kBwdThreads) {
-    const int arr = e / (N * kRowQ), rem = e % (N * kRowQ), n = rem / kRowQ, q = rem % kRowQ;
-    const int t0 = cb + q * kEl;
-    const bool ok = t0 < L;
-    const T* src = (arr == 0 ? Bp : Cp) + (int64_t)n * L + (ok ? t0 : 0);
-    cp_async16(&(arr == 0 ? rw.B : rw.C)[n][q * kEl], src, ok ? 16 : 0);
-  }
-  for (int e = threadIdx.x; e < kChunk / 4; e += kBwdThreads) {
-    const int t0 = cb + 4 * e;
-    const bool ok = t0 < L;
-    cp_async16(&rw.pos[4 * e], a.pos + (int64_t)r * L + (ok ? t0 : 0), ok ? 16 : 0);
-  }
-  if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
-    for (int e = threadIdx.x; e < N * (kBwdCh / 4); e += kBwdThreads) {
-      const int n = e / (kBwdCh / 4), q = e % (kBwdCh / 4);
-      const int d0 = dblk * kBwdCh + 4 * q;
-      const bool ok = d0 < Dn;
-      const float* src = a.states + (((int64_t)r * a.nchunk + c) * N + n) * Dn + (ok ? d0 : 0);
-      cp_async16(&rw.st[n][4 * q], src, ok ? 16 : 0);
-    }
-  }
-  cp_async_commit();
-}
-
-template <typename T, int N, bool kVec, int MinB, bool kGate>
-__global__ void __launch_bounds__(kBwdThreads, MinB)
-scan_bwd_kernel(const ScanBwdArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  using SM = BwdSmem<T, N, kGate>;
-  constexpr int NH = SM::NH, kQ = SM::kQ, kRows = SM::kRows;
-  SM& sm = *reinterpret_cast<SM*>(smem_raw);
-
-  const int L = a.L, Dn = a.Dn;
-  const int tid = threadIdx.x, lid = tid & 31, wid = tid >> 5;
-  const int cl = tid >> 1, hf = tid & 1;
-  const int n0 = hf * NH;  // first state of this thread
-  const int ndblk = (Dn + kBwdCh - 1) / kBwdCh;
-  // the chunk's per-step states live in tensor memory (one TMEM lane per
-  // thread, kChunk * NH fp32 columns: 128 at N = 16, so 4 CTAs fill the
-  // SM's 512 columns) instead of registers or shared memory.
-  constexpr uint32_t kTmemCols = (kChunk * NH <= 32) ? 32u : (kChunk * NH <= 64 ? 64u : 128u);
-  if (wid == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
-  tmem_fence_before();
-  __syncthreads();
-  tmem_fence_after();
-  const uint32_t tbase = sm.tmem_base + ((uint32_t)((wid & 3) * 32) << 16);
-
-  for (int iter = 0;; ++iter) {
-  int r, k, dblk, s0, s1;
-  if (a.items != nullptr) {  // persistent: longest segments first
-    __syncthreads();
-    if (tid == 0) sm.s_red[0] = atomicAdd(a.counter, 1);
-    __syncthreads();
-    const int w = sm.s_red[0];
-    __syncthreads();
-    if (w >= a.n_items * ndblk) break;
-    const int4 it = a.items[w / ndblk];
-    r = it.x;
-    k = it.y;
-    dblk = w % ndblk;
-    s0 = it.z;
-    s1 = it.w;
-  } else {
-    if (iter > 0) break;
-    r = blockIdx.y;
-    k = blockIdx.z;
-    dblk = blockIdx.x;
-    segment_bounds(a.pos + (int64_t)r * L, L, k, a.nseg, sm.s_red, s0, s1);
-  }
-  const int d_raw = dblk * kBwdCh + cl;
-  const bool active = d_raw < Dn;
-  const int d = active ? d_raw : Dn - 1;
-  const int32_t* pos_row = a.pos + (int64_t)r * L;
-  float* wsp = a.ws_param + (int64_t)(r * a.nseg + k) * (N + 2) * Dn;
-  if (s0 >= s1) {
-    if (active) {
-#pragma unroll
-      for (int j = 0; j < NH; ++j) wsp[(int64_t)(n0 + j) * Dn + d] = 0.f;
-      if (hf == 0) {
-        wsp[(int64_t)N * Dn + d] = 0.f;
-        wsp[(int64_t)(N + 1) * Dn + d] = 0.f;
-      }
-    }
-    continue;
-  }
-
-  const T* B_r = static_cast<const T*>(a.B) + (int64_t)r * N * L;
-  const T* C_r = static_cast<const T*>(a.C) + (int64_t)r * N * L;
-  const int64_t lane = ((int64_t)r * Dn + d) * L;
-  const T* u_row = static_cast<const T*>(a.u) + lane;
-  const T* dt_row = static_cast<const T*>(a.dt) + lane;
-  const T* dy_row = static_cast<const T*>(a.dy) + lane;
-  T* du_row = static_cast<T*>(a.du) + lane;
-  T* ddt_row = static_cast<T*>(a.ddt) + lane;
-  float* ws_bc_r = a.ws_bc + ((int64_t)dblk * a.R + r) * (int64_t)L * (2 * N);
-
-  // a thread's NH states are processed in pairs with packed fp32x2 (FFMA2)
-  constexpr int NP = NH / 2;
-  float2 A2[NP], g[NP], dA[NP];
-#pragma unroll
-  for (int p = 0; p < NP; ++p) {
-    A2[p] = make_float2(__ldg(a.A + (int64_t)d * N + n0 + 2 * p) * kLog2e,
-                        __ldg(a.A + (int64_t)d * N + n0 + 2 * p + 1) * kLog2e);
-    g[p] = make_float2(0.f, 0.f);
-    dA[p] = make_float2(0.f, 0.f);
-  }
-  const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
-  const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
-  float dD = 0.f, ddtb = 0.f;
-
-  const int cfirst = s0 / kChunk, clast = (s1 - 1) / kChunk;
-  if constexpr (kVec) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, clast, s0);
-  if (s1 == L && a.dh_last != nullptr) {  // NEXT-2: cotangent of the carried-out state
-    const float* gp = a.dh_last + ((int64_t)r * Dn + d) * N + n0;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) g[p] = make_float2(__ldg(gp + 2 * p), __ldg(gp + 2 * p + 1));
-  }
-  const T* z_row = kGate ? static_cast<const T*>(a.z) + lane : nullptr;
-  T* dz_row = kGate ? static_cast<T*>(a.dz) + lane : nullptr;
-
-  for (int c = clast; c >= cfirst; --c) {
-    const int cb = c * kChunk, c0 = max(cb, s0), c1 = min(cb + kChunk, s1);
-    if constexpr (kVec) cp_async_wait_all();
-    __syncthreads();  // raw chunk visible; previous chunk's smem readers done
-    // ---- phase 1: scalars, B/C, head, chunk start state ----
-    float2 h[NP];
-    {
-      float uu[8], vv[8], yy[8], zz[8];
-      if constexpr (kVec) {
-        const T* ru = &sm.raw.u[cl][8 * hf];
-        const T* rt = &sm.raw.dt[cl][8 * hf];
-        const T* ry = &sm.raw.dy[cl][8 * hf];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          uu[i] = IO<T>::cvt(ru[i]);
-          vv[i] = IO<T>::cvt(rt[i]);
-          yy[i] = IO<T>::cvt(ry[i]);
-          if constexpr (kGate) zz[i] = IO<T>::cvt(sm.raw.z[cl][8 * hf + i]);
-        }
-      } else {
-        load8<T, false>(u_row, cb + 8 * hf, L, uu);
-        load8<T, false>(dt_row, cb + 8 * hf, L, vv);
-        load8<T, false>(dy_row, cb + 8 * hf, L, yy);
-        if constexpr (kGate) load8<T, false>(z_row, cb + 8 * hf, L, zz);
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int ii = 8 * hf + i;
-        const float v = vv[i] + bias;
-        float dl = v, sg = 1.f;
-        if (a.softplus) {
-          float x;
-          dl = softplus_x(v, x);
-          sg = v > 20.f ? 1.f : __fdividef(x, 1.f + x);
-        }
-        float dyv = yy[i];
-        if constexpr (kGate) {  // out = y silu(z): dy = dout silu(z), dz = dout silu'(z) y
-          const float sz = sigmoidf_fast(zz[i]);
-          dyv = yy[i] * zz[i] * sz;
-          sm.sgz[ii][cl] = active ? yy[i] * sz * fmaf(zz[i], 1.f - sz, 1.f) : 0.f;
-        }
-        sm.sc[ii][cl] = make_float4(dl, active ? uu[i] : 0.f, active ? dyv : 0.f, sg);
-      }
-      if constexpr (kVec) {
-        for (int e = tid; e < N * kChunk; e += kBwdThreads) {
-          const int n = e % N, t = e / N;
-          sm.B[t][n] = IO<T>::cvt(sm.raw.B[n][t]);
-          sm.C[t][n] = IO<T>::cvt(sm.raw.C[n][t]);
-        }
-        if (tid < 32) {
-          const int t = cb + tid;
-          const bool f = tid < kChunk && (t >= L || (t == 0 && a.h0 == nullptr) ||
-                                          sm.raw.pos[tid & (kChunk - 1)] == 0);
-          const unsigned m = __ballot_sync(0xffffffffu, f);
-          if (tid == 0) sm.hmask[0] = m;
-        }
-        if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
-#pragma unroll
-          for (int p = 0; p < NP; ++p)
-            h[p] = make_float2(sm.raw.st[n0 + 2 * p][cl], sm.raw.st[n0 + 2 * p + 1][cl]);
-        } else {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
-        }
-      } else {
-        stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.hmask,
-                                      a.h0 == nullptr);
-        if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
-          const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
-#pragma unroll
-          for (int p = 0; p < NP; ++p)
-            h[p] = make_float2(st[(int64_t)(2 * p) * Dn], st[(int64_t)(2 * p + 1) * Dn]);
-        } else {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
-        }
-      }
-    }
-    __syncthreads();  // scalars visible; raw buffer free
-    const uint32_t hmask = sm.hmask[0];  // head flags of the chunk (CTA-uniform register)
-    if constexpr (kVec) {
-      if (c > cfirst) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, c - 1, s0);
-    }
-
-    auto passes = [&](auto full_tag) {
-      constexpr bool kFull = decltype(full_tag)::value;
-    // ---- pass A: forward over the chunk; the state entering step ii is kept
-    //      in TMEM columns [ii*NH, ii*NH + NH) of my lane ----
-    auto stepA = [&](const int ii) {
-      const int t = cb + ii;
-      tmem_st<NH>(tbase + (uint32_t)(ii * NH), reinterpret_cast<const float*>(h));
-      if (!kFull && (t < c0 || t >= c1)) return;  // CTA-uniform
-      const float4 scv = sm.sc[ii][cl];
-      const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
-      const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
-      if ((hmask >> ii) & 1u) {
-#pragma unroll
-        for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
-      } else {
-#pragma unroll
-        for (int p = 0; p < NP; ++p) h[p] = ffma2(ex2x2(fmul2(dl2, A2[p])), h[p], fmul2(dux2, Bt[p]));
-      }
-    };
-    if constexpr (kFull) {
-#pragma unroll
-      for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
-    } else {
-#pragma unroll 1
-      for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
-    }
-    tmem_wait_st();  // states are in TMEM before pass B reads them
-    // ---- pass B: reverse over 2-step rounds (= one reduction round).  h
-    //      holds the state after the round's last step; the states entering
-    //      its steps come from TMEM, so nothing is recomputed forward:
-    //        g += C dy;  S += g B;  dB <- g du;  dC <- dy h_t;
-    //        g <- abar_t g  (carry, 0 at heads);  q = g h_{t-1}  (= g_t abar_t h_{t-1})
-    //        dA += delta q;  dq += A q ----
-    auto sub_chunk = [&](const int sc) {
-      const int a0 = cb + sc * kBSub;
-      float2 hp[kBSub][NP];  // states entering steps a0 .. a0+kBSub-1
-      tmem_ld<kBSub * NH>(tbase + (uint32_t)(sc * kBSub * NH), reinterpret_cast<float*>(hp));
-      if (!kFull && (a0 >= c1 || a0 + kBSub <= c0)) {  // CTA-uniform
-#pragma unroll
-        for (int p = 0; p < NP; ++p) h[p] = hp[0][p];
-        return;
-      }
-      float duo[kBSub], ddo[kBSub], dzo[kBSub];
-#pragma unroll
-      for (int i = kBSub - 1; i >= 0; --i) {
-        const int t = a0 + i, ii = t - cb;
-        // row (i*kQ + q), column lid: row-wise writes are conflict-free
-        auto rslot = [&](int q) -> float4& { return sm.red[wid][i * kQ + q][lid]; };
-        const float2* hc = i == kBSub - 1 ? h : hp[i + 1];  // state after step t
-        if (!kFull && (t < c0 || t >= c1)) {  // CTA-uniform
-#pragma unroll
-          for (int q = 0; q < kQ; ++q) rslot(q) = make_float4(0.f, 0.f, 0.f, 0.f);
-          duo[i] = 0.f;
-          ddo[i] = 0.f;
-          dzo[i] = 0.f;
-          continue;
-        }
-        const float4 scv = sm.sc[ii][cl];
-        const float delta = scv.x, ux = scv.y, dyv = scv.z;
-        const float2 dl2 = f2(delta), dux2 = f2(delta * ux), dy2 = f2(dyv);
-        const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
-        const float2* Ct = reinterpret_cast<const float2*>(&sm.C[ii][n0]);
-        float2 Sp = make_float2(0.f, 0.f), dqp = make_float2(0.f, 0.f);
-        float2 vals[2 * NP];  // [dB of my NH states | dC of my NH states]
-        if ((hmask >> ii) & 1u) {  // head: abar = 0, no carry, no dA / dq term
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            g[p] = ffma2(Ct[p], dy2, g[p]);
-            Sp = ffma2(g[p], Bt[p], Sp);
-            vals[p] = fmul2(g[p], dux2);
-            vals[NP + p] = fmul2(dy2, hc[p]);
-            g[p] = make_float2(0.f, 0.f);
-          }
-        } else {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            g[p] = ffma2(Ct[p], dy2, g[p]);
-            Sp = ffma2(g[p], Bt[p], Sp);
-            vals[p] = fmul2(g[p], dux2);
-            vals[NP + p] = fmul2(dy2, hc[p]);
-            g[p] = fmul2(ex2x2(fmul2(dl2, A2[p])), g[p]);  // carry to t-1
-            const float2 q = fmul2(g[p], hp[i][p]);
-            dA[p] = ffma2(dl2, q, dA[p]);
-            dqp = ffma2(A2[p], q, dqp);
-          }
-        }
-        float Ssum = Sp.x + Sp.y, dq = dqp.x + dqp.y;
-        if constexpr (kGate) {  // y_t = C_t . h_t + D u_t (pre-gate) for dz
-          float2 yp = make_float2(0.f, 0.f);
-#pragma unroll
-          for (int p = 0; p < NP; ++p) yp = ffma2(Ct[p], hc[p], yp);
-          float yv = yp.x + yp.y;
-          yv += __shfl_xor_sync(0xffffffffu, yv, 1);
-          dzo[i] = fmaf(Dd, ux, yv) * sm.sgz[ii][cl];
-        }
-#pragma unroll
-        for (int q = 0; q < kQ; ++q)
-          rslot(q) = make_float4(vals[2 * q].x, vals[2 * q].y, vals[2 * q + 1].x, vals[2 * q + 1].y);
-        Ssum += __shfl_xor_sync(0xffffffffu, Ssum, 1);
-        dq += __shfl_xor_sync(0xffffffffu, dq, 1);
-        duo[i] = fmaf(Dd, dyv, delta * Ssum);
-        ddo[i] = fmaf(ux, Ssum, dq * kLn2) * scv.w;
-        dD = fmaf(dyv, ux, dD);
-        ddtb += ddo[i];
-      }
-#pragma unroll
-      for (int p = 0; p < NP; ++p) h[p] = hp[0][p];
-      // warp transpose-reduce of the round: lane -> (row, half, column half)
-      __syncwarp();
-      {
-        const int row = lid >> 2, rh = lid & 1, ch = (lid >> 1) & 1;
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (row < kRows) {
-          // columns 4m + (2ch + rh), m = 0..7; odd rows walk m in (m ^ 1)
-          // order so the two rows of an 8-lane phase hit disjoint banks
-          const float4* rp = &sm.red[wid][row][2 * ch + rh];
-          const int o = (row & 1) << 2;
-          float4 p0 = rp[0 ^ o], p1 = rp[4 ^ o], p2 = rp[8 ^ o], p3 = rp[12 ^ o];
-          float4 p4 = rp[16 ^ o], p5 = rp[20 ^ o], p6 = rp[24 ^ o], p7 = rp[28 ^ o];
-          auto lo = [](float4 v) { return make_float2(v.x, v.y); };
-          auto hi = [](float4 v) { return make_float2(v.z, v.w); };
-          const float2 sl = fadd2(fadd2(fadd2(lo(p0), lo(p1)), fadd2(lo(p2), lo(p3))),
-                                  fadd2(fadd2(lo(p4), lo(p5)), fadd2(lo(p6), lo(p7))));
-          const float2 sh = fadd2(fadd2(fadd2(hi(p0), hi(p1)), fadd2(hi(p2), hi(p3))),
-                                  fadd2(fadd2(hi(p4), hi(p5)), fadd2(hi(p6), hi(p7))));
-          acc = make_float4(sl.x, sl.y, sh.x, sh.y);
-        }
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
-        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
-        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 2);
-        if (row < kRows && ch == 0) sm.xw[sc][wid][row][rh] = acc;
-      }
-      __syncwarp();
-      if (active && hf == 0) {
-        if (kFull) {
-          store2<T, kVec>(du_row, a0, a0, a0 + kBSub, duo);
-          store2<T, kVec>(ddt_row, a0, a0, a0 + kBSub, ddo);
-          if constexpr (kGate) store2<T, kVec>(dz_row, a0, a0, a0 + kBSub, dzo);
-        } else {
-          store2<T, kVec>(du_row, a0, c0, c1, duo);
-          store2<T, kVec>(ddt_row, a0, c0, c1, ddo);
-          if constexpr (kGate) store2<T, kVec>(dz_row, a0, c0, c1, dzo);
-        }
-      }
-    };
-    if constexpr (kFull) {
-#pragma unroll 2
-      for (int sc = kBNSub - 1; sc >= 0; --sc) sub_chunk(sc);
-    } else {
-#pragma unroll 1
-      for (int sc = kBNSub - 1; sc >= 0; --sc) sub_chunk(sc);
-    }
-    };
-    if (c0 == cb && c1 == cb + kChunk) passes(std::true_type{});
-    else passes(std::false_type{});
-    // ---- cross-warp sum of the chunk's dB/dC partials: one barrier ----
-    __syncthreads();
-    {
-      const float* xwf = reinterpret_cast<const float*>(&sm.xw[0][0][0][0]);
-      constexpr int kWStride = kRows * 2 * 4;  // floats between warps
-      for (int e = tid; e < kChunk * 2 * N; e += kBwdThreads) {
-        const int s16 = e / (2 * N), v = e % (2 * N);
-        const int t = cb + s16;
-        if (t >= c0 && t < c1) {
-          const int n = v < N ? v : v - N;
-          const int rh = n / NH;
-          const int kk = (v < N ? 0 : NH) + n % NH;
-          const int row = (s16 & 1) * kQ + kk / 4;
-          const float* p = xwf + ((((s16 >> 1) * kBwdWarps) * kRows + row) * 2 + rh) * 4 + (kk & 3);
-          float acc = 0.f;
-#pragma unroll
-          for (int w = 0; w < kBwdWarps; ++w) acc += p[w * kWStride];
-          ws_bc_r[(int64_t)t * (2 * N) + v] = acc;
-        }
-      }
-    }
-  }
-  if (active) {
-#pragma unroll
-    for (int p = 0; p < NP; ++p) {
-      wsp[(int64_t)(n0 + 2 * p) * Dn + d] = dA[p].x;
-      wsp[(int64_t)(n0 + 2 * p + 1) * Dn + d] = dA[p].y;
-    }
-    if (hf == 0) {
-      wsp[(int64_t)N * Dn + d] = dD;
-      wsp[(int64_t)(N + 1) * Dn + d] = ddtb;
-    }
-    if (s0 == 0 && a.dh0 != nullptr) {  // NEXT-2: g now holds abar_0 g_0 = dL/dh0
-      float* gp = a.dh0 + ((int64_t)r * Dn + d) * N + n0;
-#pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        gp[2 * p] = g[p].x;
-        gp[2 * p + 1] = g[p].y;
-      }
-    }
-  }
-  }  // work loop
-  tmem_fence_before();
-  __syncthreads();
-  if (wid == 0) {
-    tmem_fence_after();
-    tmem_dealloc(sm.tmem_base, kTmemCols);
-  }
-}
-
-// dB[r,n,t] = sum_blk ws_bc[blk,r,t,n]; dC with n + N.  Fixed summation order.
-template <int N>
-__global__ void __launch_bounds__(256)
-scan_bwd_finalize_bc(const float* __restrict__ ws_bc, float* __restrict__ dB,
-                     float* __restrict__ dC, int nblk, int R, int L) {
-  constexpr int TT = 32;
-  __shared__ float tile[2 * N][TT + 1];
-  const int r = blockIdx.y, t0 = blockIdx.x * TT;
-  for (int e = threadIdx.x; e < TT * 2 * N; e += blockDim.x) {
-    const int tt = e / (2 * N), v = e % (2 * N), t = t0 + tt;
-    float s = 0.f;
-    if (t < L)
-      for (int b = 0; b < nblk; ++b)
-        s += ws_bc[(((int64_t)b * R + r) * L + t) * (2 * N) + v];
-    tile[v][tt] = s;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < TT * 2 * N; e += blockDim.x) {
-    const int v = e / TT, tt = e % TT, t = t0 + tt;
-    if (t < L) {
-      float* dst = v < N ? dB + ((int64_t)r * N + v) * L : dC + ((int64_t)r * N + (v - N)) * L;
-      dst[t] = tile[v][tt];
-    }
-  }
-}
-
-// dA[d,n], dD[d], ddt_bias[d] = sum over (row, segment) partials.
-template <int N>
-__global__ void __launch_bounds__(256)
-scan_bwd_finalize_param(const float* __restrict__ ws, float* __restrict__ dA,
-                        float* __restrict__ dD, float* __restrict__ ddtb, int nrs, int Dn) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)(N + 2) * Dn) return;
-  const int n = (int)(e / Dn), d = (int)(e % Dn);
-  float s = 0.f;
-  for (int i = 0; i < nrs; ++i) s += ws[((int64_t)i * (N + 2) + n) * Dn + d];
-  if (n < N) dA[(int64_t)d * N + n] = s;
-  else if (n == N) { if (dD) dD[d] = s; }
-  else { if (ddtb) ddtb[d] = s; }
-}
-
-}  // namespace pm
-
-// ===========================================================================
-// host side
-// ===========================================================================
 namespace {
 
 using namespace pm;
-
-int n_chunks(int64_t L) { return (int)((L + kChunk - 1) / kChunk); }
-int n_dblk(int64_t Dn) { return (int)((Dn + kScanThreads - 1) / kScanThreads); }
-int n_dblk_bwd(int64_t Dn) { return (int)((Dn + kBwdCh - 1) / kBwdCh); }
-
-// Segments per row: nominal cut every 256 steps (cuts snap to heads, so with
-// the paper's length distribution a segment is ~one sequence), <= 64.
-int n_seg(int64_t L) { return (int)std::max<int64_t>(1, std::min<int64_t>(64, L / 256)); }
-
-// states buffer = fp32 chunk states | 256 B counters | sorted segment list |
-// unsorted segment list (the fwd writes the schedule; the bwd reuses it)
-size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
-size_t states_f32_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
-  return (size_t)R * n_chunks(L) * N * Dn * sizeof(float);
-}
-size_t sched_bytes(int64_t R, int64_t L) { return 256 + 2 * up256((size_t)R * n_seg(L) * 16); }
-size_t state_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
-  return up256(states_f32_bytes(R, Dn, L, N)) + sched_bytes(R, L);
-}
-struct Sched {
-  int* counters;
-  int4* sorted;
-  int4* unsorted;
-};
-Sched sched_of(void* states, int64_t R, int64_t Dn, int64_t L, int32_t N) {
-  char* b = static_cast<char*>(states) + up256(states_f32_bytes(R, Dn, L, N));
-  Sched sc;
-  sc.counters = reinterpret_cast<int*>(b);
-  sc.sorted = reinterpret_cast<int4*>(b + 256);
-  sc.unsorted = reinterpret_cast<int4*>(b + 256 + up256((size_t)R * n_seg(L) * 16));
-  return sc;
-}
-
-bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-pm_status check_common(int64_t R, int64_t Dn, int64_t L, int32_t N, pm_dtype io) {
-  if (R < 1 || Dn < 1 || L < 1) return PM_ERR_INVALID_ARG;
-  if (io != PM_F32 && io != PM_BF16) return PM_ERR_DTYPE;
-  if (N != 4 && N != 8 && N != 16) return PM_ERR_UNSUPPORTED;
-  if (R * L >= (int64_t(1) << 31) || Dn >= (int64_t(1) << 31)) return PM_ERR_SHAPE;
-  if (R > 65535 || R * n_seg(L) * ((Dn + kBwdCh - 1) / kBwdCh) >= (int64_t(1) << 31)) return PM_ERR_SHAPE;
-  return PM_OK;
-}
-
-bool elem_aligned(const void* p, pm_dtype io) {
-  const uintptr_t m = io == PM_F32 ? 3u : 1u;
-  return p == nullptr || (reinterpret_cast<uintptr_t>(p) & m) == 0;
-}
-
-// persistent grid: resident CTAs on all SMs, capped by the number of items
-template <typename K>
-int persistent_grid(K kern, int threads, size_t smem, int64_t items) {
-  int dev = 0, nsm = 148, nb = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
-  const int64_t g = (int64_t)nsm * std::max(nb, 1);
-  if (getenv("PM_DEBUG"))
-    fprintf(stderr, "[pm] persistent grid: nsm=%d blocks/SM=%d (err=%d) smem=%zu items=%lld -> %lld\n",
-            nsm, nb, (int)e, smem, (long long)items, (long long)std::min<int64_t>(g, items));
-  return (int)std::max<int64_t>(1, std::min<int64_t>(g, items));
-}
-
-template <typename T, int N, bool kVec, int MinB, bool kGate>
-void fwd_go(const ScanFwdArgs& a, cudaStream_t s) {
-  auto kern = scan_fwd_kernel<T, N, kVec, MinB, kGate>;
-  if (a.items != nullptr) {
-    const int g = persistent_grid(kern, kScanThreads, 0, (int64_t)a.n_items * n_dblk(a.Dn));
-    kern<<<g, kScanThreads, 0, s>>>(a);
-  } else {
-    kern<<<dim3(n_dblk(a.Dn), a.R, a.nseg), kScanThreads, 0, s>>>(a);
-  }
-}
-
-template <typename T, int N, bool kVec>
-pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
-  if (a.items != nullptr) {  // schedule: plan + sort (reads pos only), reset counter
-    Sched sc = sched_of(a.states, a.R, a.Dn, a.L, N);
-    if (cudaMemsetAsync(sc.counters, 0, 256, s) != cudaSuccess) return PM_ERR_CUDA;
-    seg_plan_kernel<<<a.R, 256, 0, s>>>(a.pos, a.L, a.nseg, sc.unsorted);
-    PM_LAUNCH_CHECK();
-    seg_sort_kernel<<<1, 1024, 0, s>>>(sc.unsorted, a.n_items, a.L, sc.sorted);
-    PM_LAUNCH_CHECK();
-  }
-  if (a.z != nullptr) fwd_go<T, N, kVec, kFwdMinB, true>(a, s);
-  else fwd_go<T, N, kVec, kFwdMinB, false>(a, s);
-  PM_LAUNCH_CHECK();
-  return PM_OK;
-}
-
-template <typename T, int N>
-pm_status dispatch_fwd_vec(const ScanFwdArgs& a, bool vec, cudaStream_t s) {
-  return vec ? launch_fwd<T, N, true>(a, s) : launch_fwd<T, N, false>(a, s);
-}
-
-template <typename T>
-pm_status dispatch_fwd(const ScanFwdArgs& a, int N, bool vec, cudaStream_t s) {
-  switch (N) {
-    case 4: return dispatch_fwd_vec<T, 4>(a, vec, s);
-    case 8: return dispatch_fwd_vec<T, 8>(a, vec, s);
-    default: return dispatch_fwd_vec<T, 16>(a, vec, s);
-  }
-}
-
-template <typename T, int N, bool kVec, bool kGate>
-pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
-  const size_t smem = sizeof(BwdSmem<T, N, kGate>);
-  auto kern = scan_bwd_kernel<T, N, kVec, kBwdMinB, kGate>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return PM_ERR_CUDA;
-  // prefer the maximum shared-memory carveout so 4 CTAs (54 KB each) fit per SM
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
-    return PM_ERR_CUDA;
-  if (a.items != nullptr) {
-    if (cudaMemsetAsync(a.counter, 0, sizeof(int), s) != cudaSuccess) return PM_ERR_CUDA;
-    // resident CTAs per SM: register cap (launch bounds) and 228 KB of shared
-    // memory per SM (1 KB reserved per CTA); the occupancy API under-reports
-    // this kernel, so the grid is sized from the limits directly.
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int nb = std::max(1, std::min<int>(kBwdMinB, (int)((228 * 1024) / (smem + 1024))));
-    const int64_t items = (int64_t)a.n_items * n_dblk_bwd(a.Dn);
-    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * nb, items));
-    if (getenv("PM_DEBUG"))
-      fprintf(stderr, "[pm] bwd persistent grid: %d x %d CTAs/SM (smem %zu) -> %d\n", nsm, nb, smem, g);
-    kern<<<g, kBwdThreads, smem, s>>>(a);
-  } else {
-    kern<<<dim3(n_dblk_bwd(a.Dn), a.R, a.nseg), kBwdThreads, smem, s>>>(a);
-  }
-  PM_LAUNCH_CHECK();
-  return PM_OK;
-}
-
-template <typename T, int N, bool kVec>
-pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, float* dD,
-                     float* ddtb, cudaStream_t s) {
-  const pm_status st = a.z != nullptr ? launch_bwd_k<T, N, kVec, true>(a, s)
-                                      : launch_bwd_k<T, N, kVec, false>(a, s);
-  if (st != PM_OK) return st;
-  dim3 g2((a.L + 31) / 32, a.R);
-  scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
-  PM_LAUNCH_CHECK();
-  const int64_t np = (int64_t)(N + 2) * a.Dn;
-  scan_bwd_finalize_param<N><<<(unsigned)((np + 255) / 256), 256, 0, s>>>(
-      a.ws_param, dA, dD, ddtb, a.R * a.nseg, a.Dn);
-  PM_LAUNCH_CHECK();
-  return PM_OK;
-}
-
-template <typename T, int N>
-pm_status dispatch_bwd_vec(const ScanBwdArgs& a, bool vec, float* dA, float* dB, float* dC,
-                           float* dD, float* ddtb, cudaStream_t s) {
-  return vec ? launch_bwd<T, N, true>(a, dA, dB, dC, dD, ddtb, s)
-             : launch_bwd<T, N, false>(a, dA, dB, dC, dD, ddtb, s);
-}
-
-template <typename T>
-pm_status dispatch_bwd(const ScanBwdArgs& a, int N, bool vec, float* dA, float* dB, float* dC,
-                       float* dD, float* ddtb, cudaStream_t s) {
-  switch (N) {
-    case 4: return dispatch_bwd_vec<T, 4>(a, vec, dA, dB, dC, dD, ddtb, s);
-    case 8: return dispatch_bwd_vec<T, 8>(a, vec, dA, dB, dC, dD, ddtb, s);
-    default: return dispatch_bwd_vec<T, 16>(a, vec, dA, dB, dC, dD, ddtb, s);
-  }
-}
 
 // bwd workspace = dB/dC partials | param partials | counter | (recomputed states)
 size_t ws_bc_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
@@ -1090,8 +36,9 @@ size_t pm_selective_scan_bwd_workspace(int64_t R, int64_t Dn, int64_t L, int32_t
 
 pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt, const float* A,
                                    const void* B, const void* C, const float* Dskip,
-                                   const float* dt_bias, int32_t dt_softplus, const int32_t* pos,
-                                   const void* z, const float* h0, void* out, float* states,
+                                   const float* dt_bias, int32_t dt_softplus, int32_t zoh,
+                                   const int32_t* pos, const void* z, const float* h0, void* out,
+                                   float* states,
                                    float* h_last, int64_t R, int64_t Dn, int64_t L, int32_t N,
                                    pm_dtype io, pm_stream_t stream) {
   pm_status st = check_common(R, Dn, L, N, io);
@@ -1108,7 +55,7 @@ pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt, const float* A
                    aligned16(C) && aligned16(out) && aligned16(z);
   ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, out, states, nullptr, nullptr, 0,
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
-                z, h0, h_last};
+                z, h0, h_last, zoh ? 1 : 0};
   if (states != nullptr) {  // persistent longest-first schedule lives in the states buffer
     Sched sc = sched_of(states, R, Dn, L, N);
     a.items = sc.sorted;
@@ -1116,7 +63,7 @@ pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt, const float* A
     a.n_items = (int)(R * n_seg(L));
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  return io == PM_F32 ? dispatch_fwd<float>(a, N, vec, s) : dispatch_fwd<__nv_bfloat16>(a, N, vec, s);
+  return run_scan_fwd(a, (int)N, vec, io, s);
 }
 
 pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, const void* B,
@@ -1125,13 +72,14 @@ pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, c
                                 int64_t R, int64_t Dn, int64_t L, int32_t N, pm_dtype io,
                                 pm_stream_t stream) {
   if (!y && !states) return PM_ERR_INVALID_ARG;
-  return pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, pos, nullptr,
+  return pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, 0, pos, nullptr,
                                   nullptr, y, states, nullptr, R, Dn, L, N, io, stream);
 }
 
 pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A, const void* B,
                                    const void* C, const float* Dskip, const float* dt_bias,
-                                   int32_t dt_softplus, const int32_t* pos, const void* z,
+                                   int32_t dt_softplus, int32_t zoh, const int32_t* pos,
+                                   const void* z,
                                    const float* h0, const float* states, const void* dout,
                                    const float* dh_last, void* du, void* ddt, float* dA,
                                    float* dB, float* dC, float* dD, float* ddt_bias, void* dz,
@@ -1170,15 +118,14 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
     float* st_ws = reinterpret_cast<float*>(w);
     ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws, nullptr, nullptr, 0,
                    (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
-                   nullptr, h0, nullptr};
+                   nullptr, h0, nullptr, zoh ? 1 : 0};
     Sched sc = sched_of(st_ws, R, Dn, L, N);
     fa.items = sc.sorted;
     fa.counter = sc.counters;
     fa.n_items = (int)(R * n_seg(L));
     const bool fvec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
                       aligned16(C);
-    pm_status fs = io == PM_F32 ? dispatch_fwd<float>(fa, N, fvec, s)
-                                : dispatch_fwd<__nv_bfloat16>(fa, N, fvec, s);
+    pm_status fs = run_scan_fwd(fa, (int)N, fvec, io, s);
     if (fs != PM_OK) return fs;
     stp = st_ws;
   }
@@ -1187,9 +134,8 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
   ScanBwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, stp, dout, du, ddt, ws_bc, ws_par,
                 sc.sorted, counter, (int)(R * n_seg(L)),
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
-                z, h0, dh_last, dz, dh0};
-  return io == PM_F32 ? dispatch_bwd<float>(a, N, vec, dA, dB, dC, dD, ddt_bias, s)
-                      : dispatch_bwd<__nv_bfloat16>(a, N, vec, dA, dB, dC, dD, ddt_bias, s);
+                z, h0, dh_last, dz, dh0, zoh ? 1 : 0};
+  return run_scan_bwd(a, (int)N, vec, io, dA, dB, dC, dD, ddt_bias, s);
 }
 
 pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, const void* B,
@@ -1199,7 +145,7 @@ pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, c
                                 float* dC, float* dD, float* ddt_bias, void* workspace,
                                 size_t ws_bytes, int64_t R, int64_t Dn, int64_t L, int32_t N,
                                 pm_dtype io, pm_stream_t stream) {
-  return pm_selective_scan_bwd_ex(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, pos, nullptr,
+  return pm_selective_scan_bwd_ex(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, 0, pos, nullptr,
                                   nullptr, states, dy, nullptr, du, ddt, dA, dB, dC, dD, ddt_bias,
                                   nullptr, nullptr, workspace, ws_bytes, R, Dn, L, N, io, stream);
 }

@@ -1,0 +1,678 @@
+// scan_bwd.cu -- ScanOp_pack backward ("another two scan operators, where
+// modifications only require setting A-bar_{position_indices=0} -> 0",
+// P:224) and its deterministic finalize kernels.
+#include "scan_impl.cuh"
+
+namespace pm {
+
+// ---------------------------------------------------------------------------
+// backward
+// ---------------------------------------------------------------------------
+// Layout: a CTA owns kBwdCh channels of one row and one time segment; each
+// channel is served by a lane pair (lane = 2*c + hf), thread hf holding the
+// NH = N/2 states [hf*NH, hf*NH + NH) -- half the registers of a
+// one-thread-per-channel design, so 12 warps fit per SM.
+// Per chunk of kChunk steps (walked in reverse):
+//   staging: every per-chunk input (u, dt, dy rows, B, C, pos, the saved
+//            chunk state) is fetched with cp.async one chunk AHEAD into a raw
+//            shared buffer, so no global latency sits on the critical path;
+//   phase 1: per-(t,d) scalars delta, u, dy, softplus'(v) computed once into
+//            shared memory; B/C converted to fp32; head flags;
+//   pass A : forward recompute from the saved chunk state, storing the state
+//            at every kSub-step sub-chunk start (shared memory);
+//   pass B : per sub-chunk (reverse): recompute h_t, abar_t into registers,
+//            then the reverse recurrence g_t = C_t dy_t + abar_{t+1} g_{t+1}
+//            (abar = 0 at heads); sum_n terms are combined across the
+//            lane pair with one shuffle; dB/dC values are reduced over each
+//            warp's channels in 2-step rounds (warp transpose through a
+//            conflict-free padded buffer) and the per-warp partials of the
+//            whole chunk are summed across warps after ONE barrier.
+
+template <typename T, int N, bool kGate>
+struct BwdRaw {  // raw inputs of one chunk, filled by cp.async (vector path)
+  T u[kBwdCh][kChunk];
+  T dt[kBwdCh][kChunk];
+  T dy[kBwdCh][kChunk];
+  T z[kGate ? kBwdCh : 1][kChunk];
+  T B[N][kChunk];
+  T C[N][kChunk];
+  int32_t pos[kChunk];
+  float st[N][kBwdCh];
+};
+
+template <typename T, int N, bool kGate>
+struct BwdSmem {
+  static constexpr int NH = N / 2;   // states per thread
+  static constexpr int kQ = N / 4;   // float4 quads of (dB, dC) values per thread-step
+  static constexpr int kRows = 2 * kQ;  // transpose rows per 2-step round
+  BwdRaw<T, N, kGate> raw;
+  float4 sc[kChunk][kBwdCh];  // per-(t,d) scalars {delta, u, dy, softplus'(v)}
+                              // (u = dy = 0 on inactive channels; with the
+                              // gate, dy = dout * silu(z))
+  float sgz[kGate ? kChunk : 1][kBwdCh];  // dout * silu'(z) (gate only)
+  float4 red[kBwdWarps][kRows][kRedStride];
+  float4 xw[kChunk / 2][kBwdWarps][kRows][2];
+  float B[kChunk][N];
+  float C[kChunk][N];
+  unsigned hmask[1];  // head flags of the chunk (bit e = step cb + e)
+  int s_red[kBwdWarps];
+  uint32_t tmem_base;
+};
+
+// Issue the cp.async copies of chunk c's raw inputs (vector path only:
+// L*isz % 16 == 0, Dn % 4 == 0, 16-byte aligned pointers).
+template <typename T, int N, bool kGate>
+PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, int dblk, int c,
+                          int s0) {
+  constexpr int kEl = 16 / (int)sizeof(T);       // elements per 16-byte chunk
+  constexpr int kRowQ = kChunk / kEl;            // chunks per (row, chunk)
+  const int L = a.L, Dn = a.Dn, cb = c * kChunk;
+  constexpr int kTx = kBwdCh * kRowQ;
+#pragma unroll
+  for (int arr = 0; arr < (kGate ? 4 : 3); ++arr) {  // u, dt, dy (, z)
+    const T* base = static_cast<const T*>(arr == 0 ? a.u : arr == 1 ? a.dt : arr == 2 ? a.dy : a.z);
+    T(*dst)[kChunk] = arr == 0 ? rw.u : arr == 1 ? rw.dt : arr == 2 ? rw.dy : rw.z;
+    for (int e = threadIdx.x; e < kTx; e += kBwdThreads) {
+      const int ch = e / kRowQ, q = e % kRowQ;
+      const int d = dblk * kBwdCh + ch;
+      const int t0 = cb + q * kEl;
+      const bool ok = d < Dn && t0 < L;
+      const T* src = ok ? base + ((int64_t)r * Dn + d) * L + t0 : base;
+      cp_async16(&dst[ch][q * kEl], src, ok ? 16 : 0);
+    }
+  }
+  const T* Bp = static_cast<const T*>(a.B) + (int64_t)r * N * L;
+  const T* Cp = static_cast<const T*>(a.C) + (int64_t)r * N * L;
+  for (int e = threadIdx.x; e < 2 * N * kRowQ; e += kBwdThreads) {
+    const int arr = e / (N * kRowQ), rem = e % (N * kRowQ), n = rem / kRowQ, q = rem % kRowQ;
+    const int t0 = cb + q * kEl;
+    const bool ok = t0 < L;
+    const T* src = (arr == 0 ? Bp : Cp) + (int64_t)n * L + (ok ? t0 : 0);
+    cp_async16(&(arr == 0 ? rw.B : rw.C)[n][q * kEl], src, ok ? 16 : 0);
+  }
+  for (int e = threadIdx.x; e < kChunk / 4; e += kBwdThreads) {
+    const int t0 = cb + 4 * e;
+    const bool ok = t0 < L;
+    cp_async16(&rw.pos[4 * e], a.pos + (int64_t)r * L + (ok ? t0 : 0), ok ? 16 : 0);
+  }
+  if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
+    for (int e = threadIdx.x; e < N * (kBwdCh / 4); e += kBwdThreads) {
+      const int n = e / (kBwdCh / 4), q = e % (kBwdCh / 4);
+      const int d0 = dblk * kBwdCh + 4 * q;
+      const bool ok = d0 < Dn;
+      const float* src = a.states + (((int64_t)r * a.nchunk + c) * N + n) * Dn + (ok ? d0 : 0);
+      cp_async16(&rw.st[n][4 * q], src, ok ? 16 : 0);
+    }
+  }
+  cp_async_commit();
+}
+
+template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh>
+__global__ void __launch_bounds__(kBwdThreads, MinB)
+scan_bwd_kernel(const ScanBwdArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using SM = BwdSmem<T, N, kGate>;
+  constexpr int NH = SM::NH, kQ = SM::kQ, kRows = SM::kRows;
+  SM& sm = *reinterpret_cast<SM*>(smem_raw);
+
+  const int L = a.L, Dn = a.Dn;
+  const int tid = threadIdx.x, lid = tid & 31, wid = tid >> 5;
+  const int cl = tid >> 1, hf = tid & 1;
+  const int n0 = hf * NH;  // first state of this thread
+  const int ndblk = (Dn + kBwdCh - 1) / kBwdCh;
+  // the chunk's per-step states live in tensor memory (one TMEM lane per
+  // thread, kChunk * NH fp32 columns: 128 at N = 16, so 4 CTAs fill the
+  // SM's 512 columns) instead of registers or shared memory.
+  constexpr uint32_t kTmemCols = (kChunk * NH <= 32) ? 32u : (kChunk * NH <= 64 ? 64u : 128u);
+  if (wid == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = sm.tmem_base + ((uint32_t)((wid & 3) * 32) << 16);
+
+  for (int iter = 0;; ++iter) {
+  int r, k, dblk, s0, s1;
+  if (a.items != nullptr) {  // persistent: longest segments first
+    __syncthreads();
+    if (tid == 0) sm.s_red[0] = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int w = sm.s_red[0];
+    __syncthreads();
+    if (w >= a.n_items * ndblk) break;
+    const int4 it = a.items[w / ndblk];
+    r = it.x;
+    k = it.y;
+    dblk = w % ndblk;
+    s0 = it.z;
+    s1 = it.w;
+  } else {
+    if (iter > 0) break;
+    r = blockIdx.y;
+    k = blockIdx.z;
+    dblk = blockIdx.x;
+    segment_bounds(a.pos + (int64_t)r * L, L, k, a.nseg, sm.s_red, s0, s1);
+  }
+  const int d_raw = dblk * kBwdCh + cl;
+  const bool active = d_raw < Dn;
+  const int d = active ? d_raw : Dn - 1;
+  const int32_t* pos_row = a.pos + (int64_t)r * L;
+  float* wsp = a.ws_param + (int64_t)(r * a.nseg + k) * (N + 2) * Dn;
+  if (s0 >= s1) {
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < NH; ++j) wsp[(int64_t)(n0 + j) * Dn + d] = 0.f;
+      if (hf == 0) {
+        wsp[(int64_t)N * Dn + d] = 0.f;
+        wsp[(int64_t)(N + 1) * Dn + d] = 0.f;
+      }
+    }
+    continue;
+  }
+
+  const T* B_r = static_cast<const T*>(a.B) + (int64_t)r * N * L;
+  const T* C_r = static_cast<const T*>(a.C) + (int64_t)r * N * L;
+  const int64_t lane = ((int64_t)r * Dn + d) * L;
+  const T* u_row = static_cast<const T*>(a.u) + lane;
+  const T* dt_row = static_cast<const T*>(a.dt) + lane;
+  const T* dy_row = static_cast<const T*>(a.dy) + lane;
+  T* du_row = static_cast<T*>(a.du) + lane;
+  T* ddt_row = static_cast<T*>(a.ddt) + lane;
+  float* ws_bc_r = a.ws_bc + ((int64_t)dblk * a.R + r) * (int64_t)L * (2 * N);
+
+  // a thread's NH states are processed in pairs with packed fp32x2 (FFMA2)
+  constexpr int NP = NH / 2;
+  float2 A2[NP], g[NP], dA[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    A2[p] = make_float2(__ldg(a.A + (int64_t)d * N + n0 + 2 * p) * kLog2e,
+                        __ldg(a.A + (int64_t)d * N + n0 + 2 * p + 1) * kLog2e);
+    g[p] = make_float2(0.f, 0.f);
+    dA[p] = make_float2(0.f, 0.f);
+  }
+  float2 invA[kZoh ? NP : 1];  // 1/A for the ZOH factor (inf at A = 0: series branch)
+  if constexpr (kZoh) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+      invA[p] = make_float2(1.f / __ldg(a.A + (int64_t)d * N + n0 + 2 * p),
+                            1.f / __ldg(a.A + (int64_t)d * N + n0 + 2 * p + 1));
+  }
+  const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
+  const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
+  float dD = 0.f, ddtb = 0.f;
+
+  const int cfirst = s0 / kChunk, clast = (s1 - 1) / kChunk;
+  if constexpr (kVec) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, clast, s0);
+  if (s1 == L && a.dh_last != nullptr) {  // NEXT-2: cotangent of the carried-out state
+    const float* gp = a.dh_last + ((int64_t)r * Dn + d) * N + n0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) g[p] = make_float2(__ldg(gp + 2 * p), __ldg(gp + 2 * p + 1));
+  }
+  const T* z_row = kGate ? static_cast<const T*>(a.z) + lane : nullptr;
+  T* dz_row = kGate ? static_cast<T*>(a.dz) + lane : nullptr;
+
+  for (int c = clast; c >= cfirst; --c) {
+    const int cb = c * kChunk, c0 = max(cb, s0), c1 = min(cb + kChunk, s1);
+    if constexpr (kVec) cp_async_wait_all();
+    __syncthreads();  // raw chunk visible; previous chunk's smem readers done
+    // ---- phase 1: scalars, B/C, head, chunk start state ----
+    float2 h[NP];
+    {
+      float uu[8], vv[8], yy[8], zz[8];
+      if constexpr (kVec) {
+        const T* ru = &sm.raw.u[cl][8 * hf];
+        const T* rt = &sm.raw.dt[cl][8 * hf];
+        const T* ry = &sm.raw.dy[cl][8 * hf];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uu[i] = IO<T>::cvt(ru[i]);
+          vv[i] = IO<T>::cvt(rt[i]);
+          yy[i] = IO<T>::cvt(ry[i]);
+          if constexpr (kGate) zz[i] = IO<T>::cvt(sm.raw.z[cl][8 * hf + i]);
+        }
+      } else {
+        load8<T, false>(u_row, cb + 8 * hf, L, uu);
+        load8<T, false>(dt_row, cb + 8 * hf, L, vv);
+        load8<T, false>(dy_row, cb + 8 * hf, L, yy);
+        if constexpr (kGate) load8<T, false>(z_row, cb + 8 * hf, L, zz);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int ii = 8 * hf + i;
+        const float v = vv[i] + bias;
+        float dl = v, sg = 1.f;
+        if (a.softplus) {
+          float x;
+          dl = softplus_x(v, x);
+          sg = v > 20.f ? 1.f : __fdividef(x, 1.f + x);
+        }
+        float dyv = yy[i];
+        if constexpr (kGate) {  // out = y silu(z): dy = dout silu(z), dz = dout silu'(z) y
+          const float sz = sigmoidf_fast(zz[i]);
+          dyv = yy[i] * zz[i] * sz;
+          sm.sgz[ii][cl] = active ? yy[i] * sz * fmaf(zz[i], 1.f - sz, 1.f) : 0.f;
+        }
+        sm.sc[ii][cl] = make_float4(dl, active ? uu[i] : 0.f, active ? dyv : 0.f, sg);
+      }
+      if constexpr (kVec) {
+        for (int e = tid; e < N * kChunk; e += kBwdThreads) {
+          const int n = e % N, t = e / N;
+          sm.B[t][n] = IO<T>::cvt(sm.raw.B[n][t]);
+          sm.C[t][n] = IO<T>::cvt(sm.raw.C[n][t]);
+        }
+        if (tid < 32) {
+          const int t = cb + tid;
+          const bool f = tid < kChunk && (t >= L || (t == 0 && a.h0 == nullptr) ||
+                                          sm.raw.pos[tid & (kChunk - 1)] == 0);
+          const unsigned m = __ballot_sync(0xffffffffu, f);
+          if (tid == 0) sm.hmask[0] = m;
+        }
+        if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
+#pragma unroll
+          for (int p = 0; p < NP; ++p)
+            h[p] = make_float2(sm.raw.st[n0 + 2 * p][cl], sm.raw.st[n0 + 2 * p + 1][cl]);
+        } else {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
+        }
+      } else {
+        stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.hmask,
+                                      a.h0 == nullptr);
+        if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
+          const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
+#pragma unroll
+          for (int p = 0; p < NP; ++p)
+            h[p] = make_float2(st[(int64_t)(2 * p) * Dn], st[(int64_t)(2 * p + 1) * Dn]);
+        } else {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
+        }
+      }
+    }
+    __syncthreads();  // scalars visible; raw buffer free
+    const uint32_t hmask = sm.hmask[0];  // head flags of the chunk (CTA-uniform register)
+    if constexpr (kVec) {
+      if (c > cfirst) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, c - 1, s0);
+    }
+
+    auto passes = [&](auto full_tag) {
+      constexpr bool kFull = decltype(full_tag)::value;
+    // ---- pass A: forward over the chunk; the state entering step ii is kept
+    //      in TMEM columns [ii*NH, ii*NH + NH) of my lane ----
+    auto stepA = [&](const int ii) {
+      const int t = cb + ii;
+      tmem_st<NH>(tbase + (uint32_t)(ii * NH), reinterpret_cast<const float*>(h));
+      if (!kFull && (t < c0 || t >= c1)) return;  // CTA-uniform
+      const float4 scv = sm.sc[ii][cl];
+      const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
+      const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
+      if constexpr (kZoh) {  // B-bar u = f(z) delta B u (Eq 2b)
+        const bool head = (hmask >> ii) & 1u;
+        const float2 u2 = f2(scv.y);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const float2 m = fmul2(dl2, A2[p]);
+          const float2 ab = ex2x2(m);
+          const float2 zz2 = fmul2(m, f2(kLn2));
+          const float2 bf = make_float2(zoh_bfac(ab.x, zz2.x, invA[p].x, scv.x),
+                                        zoh_bfac(ab.y, zz2.y, invA[p].y, scv.x));
+          const float2 bx = fmul2(bf, fmul2(u2, Bt[p]));
+          h[p] = head ? bx : ffma2(ab, h[p], bx);
+        }
+      } else if ((hmask >> ii) & 1u) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
+      } else {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) h[p] = ffma2(ex2x2(fmul2(dl2, A2[p])), h[p], fmul2(dux2, Bt[p]));
+      }
+    };
+    if constexpr (kFull) {
+#pragma unroll
+      for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
+    } else {
+#pragma unroll 1
+      for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
+    }
+    tmem_wait_st();  // states are in TMEM before pass B reads them
+    // ---- pass B: reverse over 2-step rounds (= one reduction round).  h
+    //      holds the state after the round's last step; the states entering
+    //      its steps come from TMEM, so nothing is recomputed forward:
+    //        g += C dy;  S += g B;  dB <- g du;  dC <- dy h_t;
+    //        g <- abar_t g  (carry, 0 at heads);  q = g h_{t-1}  (= g_t abar_t h_{t-1})
+    //        dA += delta q;  dq += A q ----
+    auto sub_chunk = [&](const int sc) {
+      const int a0 = cb + sc * kBSub;
+      float2 hp[kBSub][NP];  // states entering steps a0 .. a0+kBSub-1
+      tmem_ld<kBSub * NH>(tbase + (uint32_t)(sc * kBSub * NH), reinterpret_cast<float*>(hp));
+      if (!kFull && (a0 >= c1 || a0 + kBSub <= c0)) {  // CTA-uniform
+#pragma unroll
+        for (int p = 0; p < NP; ++p) h[p] = hp[0][p];
+        return;
+      }
+      float duo[kBSub], ddo[kBSub], dzo[kBSub];
+#pragma unroll
+      for (int i = kBSub - 1; i >= 0; --i) {
+        const int t = a0 + i, ii = t - cb;
+        // row (i*kQ + q), column lid: row-wise writes are conflict-free
+        auto rslot = [&](int q) -> float4& { return sm.red[wid][i * kQ + q][lid]; };
+        const float2* hc = i == kBSub - 1 ? h : hp[i + 1];  // state after step t
+        if (!kFull && (t < c0 || t >= c1)) {  // CTA-uniform
+#pragma unroll
+          for (int q = 0; q < kQ; ++q) rslot(q) = make_float4(0.f, 0.f, 0.f, 0.f);
+          duo[i] = 0.f;
+          ddo[i] = 0.f;
+          dzo[i] = 0.f;
+          continue;
+        }
+        const float4 scv = sm.sc[ii][cl];
+        const float delta = scv.x, ux = scv.y, dyv = scv.z;
+        const float2 dl2 = f2(delta), dux2 = f2(delta * ux), dy2 = f2(dyv);
+        const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
+        const float2* Ct = reinterpret_cast<const float2*>(&sm.C[ii][n0]);
+        float2 Sp = make_float2(0.f, 0.f), dqp = make_float2(0.f, 0.f);
+        float2 Sdp = make_float2(0.f, 0.f);  // ZOH: sum_n g B e^z (d bfac / d delta)
+        float2 vals[2 * NP];  // [dB of my NH states | dC of my NH states]
+        if constexpr (kZoh) {
+          // ZOH (Eq 2b): h_t = abar h_{t-1} + bfac B u with bfac = f(z) delta:
+          //   du += g B bfac;  ddelta += u g B e^z;  dB <- g bfac u;
+          //   dA += g B u delta (delta f'(z))  (+ the abar terms as Euler)
+          const bool head = (hmask >> ii) & 1u;
+          const float2 u2 = f2(ux);
+          const float rdl = rcp(delta);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            const float2 m = fmul2(dl2, A2[p]);
+            const float2 ab = ex2x2(m);
+            const float2 zz2 = fmul2(m, f2(kLn2));
+            float2 bf, dfp;
+            zoh_coef(ab.x, zz2.x, invA[p].x, delta, rdl, bf.x, dfp.x);
+            zoh_coef(ab.y, zz2.y, invA[p].y, delta, rdl, bf.y, dfp.y);
+            g[p] = ffma2(Ct[p], dy2, g[p]);
+            const float2 gB = fmul2(g[p], Bt[p]);
+            Sp = ffma2(gB, bf, Sp);
+            Sdp = ffma2(gB, ab, Sdp);
+            vals[p] = fmul2(g[p], fmul2(bf, u2));
+            vals[NP + p] = fmul2(dy2, hc[p]);
+            dA[p] = ffma2(gB, fmul2(dux2, dfp), dA[p]);
+            if (head) {
+              g[p] = make_float2(0.f, 0.f);
+            } else {
+              g[p] = fmul2(ab, g[p]);  // carry to t-1
+              const float2 q = fmul2(g[p], hp[i][p]);
+              dA[p] = ffma2(dl2, q, dA[p]);
+              dqp = ffma2(A2[p], q, dqp);
+            }
+          }
+        } else if ((hmask >> ii) & 1u) {  // head: abar = 0, no carry, no dA / dq term
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            g[p] = ffma2(Ct[p], dy2, g[p]);
+            Sp = ffma2(g[p], Bt[p], Sp);
+            vals[p] = fmul2(g[p], dux2);
+            vals[NP + p] = fmul2(dy2, hc[p]);
+            g[p] = make_float2(0.f, 0.f);
+          }
+        } else {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            g[p] = ffma2(Ct[p], dy2, g[p]);
+            Sp = ffma2(g[p], Bt[p], Sp);
+            vals[p] = fmul2(g[p], dux2);
+            vals[NP + p] = fmul2(dy2, hc[p]);
+            g[p] = fmul2(ex2x2(fmul2(dl2, A2[p])), g[p]);  // carry to t-1
+            const float2 q = fmul2(g[p], hp[i][p]);
+            dA[p] = ffma2(dl2, q, dA[p]);
+            dqp = ffma2(A2[p], q, dqp);
+          }
+        }
+        float Ssum = Sp.x + Sp.y, dq = dqp.x + dqp.y;
+        if constexpr (kGate) {  // y_t = C_t . h_t + D u_t (pre-gate) for dz
+          float2 yp = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) yp = ffma2(Ct[p], hc[p], yp);
+          float yv = yp.x + yp.y;
+          yv += __shfl_xor_sync(0xffffffffu, yv, 1);
+          dzo[i] = fmaf(Dd, ux, yv) * sm.sgz[ii][cl];
+        }
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+          rslot(q) = make_float4(vals[2 * q].x, vals[2 * q].y, vals[2 * q + 1].x, vals[2 * q + 1].y);
+        Ssum += __shfl_xor_sync(0xffffffffu, Ssum, 1);
+        dq += __shfl_xor_sync(0xffffffffu, dq, 1);
+        if constexpr (kZoh) {  // Ssum already carries bfac (which includes delta)
+          float Sd = Sdp.x + Sdp.y;
+          Sd += __shfl_xor_sync(0xffffffffu, Sd, 1);
+          duo[i] = fmaf(Dd, dyv, Ssum);
+          ddo[i] = fmaf(ux, Sd, dq * kLn2) * scv.w;
+        } else {
+          duo[i] = fmaf(Dd, dyv, delta * Ssum);
+          ddo[i] = fmaf(ux, Ssum, dq * kLn2) * scv.w;
+        }
+        dD = fmaf(dyv, ux, dD);
+        ddtb += ddo[i];
+      }
+#pragma unroll
+      for (int p = 0; p < NP; ++p) h[p] = hp[0][p];
+      // warp transpose-reduce of the round: lane -> (row, half, column half)
+      __syncwarp();
+      {
+        const int row = lid >> 2, rh = lid & 1, ch = (lid >> 1) & 1;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < kRows) {
+          // columns 4m + (2ch + rh), m = 0..7; odd rows walk m in (m ^ 1)
+          // order so the two rows of an 8-lane phase hit disjoint banks
+          const float4* rp = &sm.red[wid][row][2 * ch + rh];
+          const int o = (row & 1) << 2;
+          float4 p0 = rp[0 ^ o], p1 = rp[4 ^ o], p2 = rp[8 ^ o], p3 = rp[12 ^ o];
+          float4 p4 = rp[16 ^ o], p5 = rp[20 ^ o], p6 = rp[24 ^ o], p7 = rp[28 ^ o];
+          auto lo = [](float4 v) { return make_float2(v.x, v.y); };
+          auto hi = [](float4 v) { return make_float2(v.z, v.w); };
+          const float2 sl = fadd2(fadd2(fadd2(lo(p0), lo(p1)), fadd2(lo(p2), lo(p3))),
+                                  fadd2(fadd2(lo(p4), lo(p5)), fadd2(lo(p6), lo(p7))));
+          const float2 sh = fadd2(fadd2(fadd2(hi(p0), hi(p1)), fadd2(hi(p2), hi(p3))),
+                                  fadd2(fadd2(hi(p4), hi(p5)), fadd2(hi(p6), hi(p7))));
+          acc = make_float4(sl.x, sl.y, sh.x, sh.y);
+        }
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
+        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 2);
+        if (row < kRows && ch == 0) sm.xw[sc][wid][row][rh] = acc;
+      }
+      __syncwarp();
+      if (active && hf == 0) {
+        if (kFull) {
+          store2<T, kVec>(du_row, a0, a0, a0 + kBSub, duo);
+          store2<T, kVec>(ddt_row, a0, a0, a0 + kBSub, ddo);
+          if constexpr (kGate) store2<T, kVec>(dz_row, a0, a0, a0 + kBSub, dzo);
+        } else {
+          store2<T, kVec>(du_row, a0, c0, c1, duo);
+          store2<T, kVec>(ddt_row, a0, c0, c1, ddo);
+          if constexpr (kGate) store2<T, kVec>(dz_row, a0, c0, c1, dzo);
+        }
+      }
+    };
+    if constexpr (kFull) {
+#pragma unroll 2
+      for (int sc = kBNSub - 1; sc >= 0; --sc) sub_chunk(sc);
+    } else {
+#pragma unroll 1
+      for (int sc = kBNSub - 1; sc >= 0; --sc) sub_chunk(sc);
+    }
+    };
+    if (c0 == cb && c1 == cb + kChunk) passes(std::true_type{});
+    else passes(std::false_type{});
+    // ---- cross-warp sum of the chunk's dB/dC partials: one barrier ----
+    __syncthreads();
+    {
+      const float* xwf = reinterpret_cast<const float*>(&sm.xw[0][0][0][0]);
+      constexpr int kWStride = kRows * 2 * 4;  // floats between warps
+      for (int e = tid; e < kChunk * 2 * N; e += kBwdThreads) {
+        const int s16 = e / (2 * N), v = e % (2 * N);
+        const int t = cb + s16;
+        if (t >= c0 && t < c1) {
+          const int n = v < N ? v : v - N;
+          const int rh = n / NH;
+          const int kk = (v < N ? 0 : NH) + n % NH;
+          const int row = (s16 & 1) * kQ + kk / 4;
+          const float* p = xwf + ((((s16 >> 1) * kBwdWarps) * kRows + row) * 2 + rh) * 4 + (kk & 3);
+          float acc = 0.f;
+#pragma unroll
+          for (int w = 0; w < kBwdWarps; ++w) acc += p[w * kWStride];
+          ws_bc_r[(int64_t)t * (2 * N) + v] = acc;
+        }
+      }
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      wsp[(int64_t)(n0 + 2 * p) * Dn + d] = dA[p].x;
+      wsp[(int64_t)(n0 + 2 * p + 1) * Dn + d] = dA[p].y;
+    }
+    if (hf == 0) {
+      wsp[(int64_t)N * Dn + d] = dD;
+      wsp[(int64_t)(N + 1) * Dn + d] = ddtb;
+    }
+    if (s0 == 0 && a.dh0 != nullptr) {  // NEXT-2: g now holds abar_0 g_0 = dL/dh0
+      float* gp = a.dh0 + ((int64_t)r * Dn + d) * N + n0;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        gp[2 * p] = g[p].x;
+        gp[2 * p + 1] = g[p].y;
+      }
+    }
+  }
+  }  // work loop
+  tmem_fence_before();
+  __syncthreads();
+  if (wid == 0) {
+    tmem_fence_after();
+    tmem_dealloc(sm.tmem_base, kTmemCols);
+  }
+}
+
+// dB[r,n,t] = sum_blk ws_bc[blk,r,t,n]; dC with n + N.  Fixed summation order.
+template <int N>
+__global__ void __launch_bounds__(256)
+scan_bwd_finalize_bc(const float* __restrict__ ws_bc, float* __restrict__ dB,
+                     float* __restrict__ dC, int nblk, int R, int L) {
+  constexpr int TT = 32;
+  __shared__ float tile[2 * N][TT + 1];
+  const int r = blockIdx.y, t0 = blockIdx.x * TT;
+  for (int e = threadIdx.x; e < TT * 2 * N; e += blockDim.x) {
+    const int tt = e / (2 * N), v = e % (2 * N), t = t0 + tt;
+    float s = 0.f;
+    if (t < L)
+      for (int b = 0; b < nblk; ++b)
+        s += ws_bc[(((int64_t)b * R + r) * L + t) * (2 * N) + v];
+    tile[v][tt] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < TT * 2 * N; e += blockDim.x) {
+    const int v = e / TT, tt = e % TT, t = t0 + tt;
+    if (t < L) {
+      float* dst = v < N ? dB + ((int64_t)r * N + v) * L : dC + ((int64_t)r * N + (v - N)) * L;
+      dst[t] = tile[v][tt];
+    }
+  }
+}
+
+// dA[d,n], dD[d], ddt_bias[d] = sum over (row, segment) partials.
+template <int N>
+__global__ void __launch_bounds__(256)
+scan_bwd_finalize_param(const float* __restrict__ ws, float* __restrict__ dA,
+                        float* __restrict__ dD, float* __restrict__ ddtb, int nrs, int Dn) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)(N + 2) * Dn) return;
+  const int n = (int)(e / Dn), d = (int)(e % Dn);
+  float s = 0.f;
+  for (int i = 0; i < nrs; ++i) s += ws[((int64_t)i * (N + 2) + n) * Dn + d];
+  if (n < N) dA[(int64_t)d * N + n] = s;
+  else if (n == N) { if (dD) dD[d] = s; }
+  else { if (ddtb) ddtb[d] = s; }
+}
+
+// ===========================================================================
+// host side
+// ===========================================================================
+namespace {
+
+template <typename T, int N, bool kVec, bool kGate, bool kZoh>
+pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
+  const size_t smem = sizeof(BwdSmem<T, N, kGate>);
+  // ZOH carries 1/A and the series: 3 CTAs/SM (168 registers) avoid spills
+  constexpr int kMinB = kZoh ? 3 : kBwdMinB;
+  auto kern = scan_bwd_kernel<T, N, kVec, kMinB, kGate, kZoh>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return PM_ERR_CUDA;
+  // prefer the maximum shared-memory carveout so 4 CTAs (54 KB each) fit per SM
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
+    return PM_ERR_CUDA;
+  if (a.items != nullptr) {
+    if (cudaMemsetAsync(a.counter, 0, sizeof(int), s) != cudaSuccess) return PM_ERR_CUDA;
+    // resident CTAs per SM: register cap (launch bounds) and 228 KB of shared
+    // memory per SM (1 KB reserved per CTA); the occupancy API under-reports
+    // this kernel, so the grid is sized from the limits directly.
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int nb = std::max(1, std::min<int>(kMinB, (int)((228 * 1024) / (smem + 1024))));
+    const int64_t items = (int64_t)a.n_items * n_dblk_bwd(a.Dn);
+    const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * nb, items));
+    if (getenv("PM_DEBUG"))
+      fprintf(stderr, "[pm] bwd persistent grid: %d x %d CTAs/SM (smem %zu) -> %d\n", nsm, nb, smem, g);
+    kern<<<g, kBwdThreads, smem, s>>>(a);
+  } else {
+    kern<<<dim3(n_dblk_bwd(a.Dn), a.R, a.nseg), kBwdThreads, smem, s>>>(a);
+  }
+  PM_LAUNCH_CHECK();
+  return PM_OK;
+}
+
+template <typename T, int N, bool kVec>
+pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, float* dD,
+                     float* ddtb, cudaStream_t s) {
+  const pm_status st =
+      a.zoh ? (a.z != nullptr ? launch_bwd_k<T, N, kVec, true, true>(a, s)
+                              : launch_bwd_k<T, N, kVec, false, true>(a, s))
+            : (a.z != nullptr ? launch_bwd_k<T, N, kVec, true, false>(a, s)
+                              : launch_bwd_k<T, N, kVec, false, false>(a, s));
+  if (st != PM_OK) return st;
+  dim3 g2((a.L + 31) / 32, a.R);
+  scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
+  PM_LAUNCH_CHECK();
+  const int64_t np = (int64_t)(N + 2) * a.Dn;
+  scan_bwd_finalize_param<N><<<(unsigned)((np + 255) / 256), 256, 0, s>>>(
+      a.ws_param, dA, dD, ddtb, a.R * a.nseg, a.Dn);
+  PM_LAUNCH_CHECK();
+  return PM_OK;
+}
+
+template <typename T, int N>
+pm_status dispatch_bwd_vec(const ScanBwdArgs& a, bool vec, float* dA, float* dB, float* dC,
+                           float* dD, float* ddtb, cudaStream_t s) {
+  return vec ? launch_bwd<T, N, true>(a, dA, dB, dC, dD, ddtb, s)
+             : launch_bwd<T, N, false>(a, dA, dB, dC, dD, ddtb, s);
+}
+
+template <typename T>
+pm_status dispatch_bwd_t(const ScanBwdArgs& a, int N, bool vec, float* dA, float* dB, float* dC,
+                       float* dD, float* ddtb, cudaStream_t s) {
+  switch (N) {
+    case 4: return dispatch_bwd_vec<T, 4>(a, vec, dA, dB, dC, dD, ddtb, s);
+    case 8: return dispatch_bwd_vec<T, 8>(a, vec, dA, dB, dC, dD, ddtb, s);
+    default: return dispatch_bwd_vec<T, 16>(a, vec, dA, dB, dC, dD, ddtb, s);
+  }
+}
+
+}  // namespace
+
+pm_status run_scan_bwd(const ScanBwdArgs& a, int N, bool vec, pm_dtype io, float* dA, float* dB,
+                       float* dC, float* dD, float* ddtb, cudaStream_t s) {
+  return io == PM_F32 ? dispatch_bwd_t<float>(a, N, vec, dA, dB, dC, dD, ddtb, s)
+                      : dispatch_bwd_t<__nv_bfloat16>(a, N, vec, dA, dB, dC, dD, ddtb, s);
+}
+
+}  // namespace pm

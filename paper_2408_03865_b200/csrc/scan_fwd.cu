@@ -1,0 +1,327 @@
+// scan_fwd.cu -- ScanOp_pack forward (Alg 2; Eq 1a/1b/2a
+// P:202-205) and the segment schedule (plan + longest-first sort).
+#include "scan_impl.cuh"
+
+namespace pm {
+
+// Work scheduling.  Segment lengths follow the sequence-length distribution
+// (57..2048 steps), so a plain grid leaves a long tail.  A planning kernel
+// lists every row's segments, one CTA sorts them longest-first, and the scan
+// kernels are persistent: each CTA pulls (segment, channel-block) items from
+// an atomic counter in that order (LPT), so the last items are the shortest.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) seg_plan_kernel(const int32_t* __restrict__ pos, int L,
+                                                      int nseg, int4* __restrict__ items) {
+  // cut k (1 <= k < nseg) = first head at or after k * ceil(L / nseg), as in
+  // segment_bounds(); one warp per cut, 32 positions per ballot
+  __shared__ int cut[65];
+  const int r = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int32_t* pos_row = pos + (int64_t)r * L;
+  const int seg = (L + nseg - 1) / nseg;
+  for (int k = 1 + warp; k < nseg; k += blockDim.x >> 5) {
+    int b = L;
+    for (int base = k * seg; base < L; base += 32) {
+      const int t = base + lane;
+      const unsigned m = __ballot_sync(0xffffffffu, t < L && __ldg(pos_row + t) == 0);
+      if (m) {
+        b = base + __ffs(m) - 1;
+        break;
+      }
+    }
+    if (lane == 0) cut[k] = min(b, L);
+  }
+  if (threadIdx.x == 0) {
+    cut[0] = 0;
+    cut[nseg] = L;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nseg; k += blockDim.x)
+    items[r * nseg + k] = make_int4(r, k, cut[k], max(cut[k], cut[k + 1]));
+}
+
+// Longest-first order of the segment list (one CTA).  n <= 4096: exact rank
+// sort (length descending, ties by index); larger n: bucket sort on 1024
+// length bins (order within a bin is arbitrary -- results never depend on
+// the processing order, only the load balance does).
+__global__ void __launch_bounds__(1024) seg_sort_kernel(const int4* __restrict__ in, int n, int L,
+                                                       int4* __restrict__ out) {
+  if (n <= 4096) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int4 a = in[i];
+      const int la = a.w - a.z;
+      int rank = 0;
+      for (int j = 0; j < n; ++j) {
+        const int4 b = in[j];
+        const int lb = b.w - b.z;
+        rank += (lb > la) || (lb == la && j < i);
+      }
+      out[rank] = a;
+    }
+    return;
+  }
+  constexpr int kBins = 1024;
+  __shared__ int cnt[kBins];
+  for (int b = threadIdx.x; b < kBins; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();
+  auto bin_of = [&](const int4 v) {  // longest first: bin 0 = longest
+    const int len = v.w - v.z;
+    return kBins - 1 - (int)(((int64_t)len * (kBins - 1)) / max(L, 1));
+  };
+  for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[bin_of(in[i])], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan -> bin cursors
+    int acc = 0;
+    for (int b = 0; b < kBins; ++b) {
+      const int c = cnt[b];
+      cnt[b] = acc;
+      acc += c;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int4 v = in[i];
+    out[atomicAdd(&cnt[bin_of(v)], 1)] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh>
+__global__ void __launch_bounds__(kScanThreads, MinB)
+scan_fwd_kernel(const ScanFwdArgs a) {
+  __shared__ __align__(16) float sB[kTile][N];
+  __shared__ __align__(16) float sC[kTile][N];
+  __shared__ unsigned sMask[kTile / 32];
+  __shared__ int s_red[kScanWarps];
+  __shared__ int s_work;
+
+  const int L = a.L, Dn = a.Dn;
+  const int ndblk = (Dn + kScanThreads - 1) / kScanThreads;
+  for (int iter = 0;; ++iter) {
+  int r, dblk, s0, s1;
+  if (a.items != nullptr) {  // persistent: longest segments first
+    __syncthreads();
+    if (threadIdx.x == 0) s_work = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int w = s_work;
+    if (w >= a.n_items * ndblk) break;
+    const int4 it = a.items[w / ndblk];
+    r = it.x;
+    dblk = w % ndblk;
+    s0 = it.z;
+    s1 = it.w;
+  } else {
+    if (iter > 0) break;
+    r = blockIdx.y;
+    dblk = blockIdx.x;
+    segment_bounds(a.pos + (int64_t)r * L, L, blockIdx.z, a.nseg, s_red, s0, s1);
+  }
+  if (s0 >= s1) continue;
+  const int d_raw = dblk * kScanThreads + threadIdx.x;
+  const bool active = d_raw < Dn;
+  const int d = active ? d_raw : Dn - 1;
+  const int32_t* pos_row = a.pos + (int64_t)r * L;
+
+  const T* B_r = static_cast<const T*>(a.B) + (int64_t)r * N * L;
+  const T* C_r = static_cast<const T*>(a.C) + (int64_t)r * N * L;
+  const int64_t lane = ((int64_t)r * Dn + d) * L;
+  const T* u_row = static_cast<const T*>(a.u) + lane;
+  const T* dt_row = static_cast<const T*>(a.dt) + lane;
+  T* y_row = a.y ? static_cast<T*>(a.y) + lane : nullptr;
+  const T* z_row = kGate ? static_cast<const T*>(a.z) + lane : nullptr;
+
+  // states are processed in pairs with packed fp32x2 arithmetic (FFMA2)
+  constexpr int NP = N / 2;
+  float2 A2[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p)
+    A2[p] = make_float2(__ldg(a.A + (int64_t)d * N + 2 * p) * kLog2e,
+                        __ldg(a.A + (int64_t)d * N + 2 * p + 1) * kLog2e);
+  float2 invA[kZoh ? NP : 1];  // 1/A for the ZOH factor (inf at A = 0: series branch)
+  if constexpr (kZoh) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+      invA[p] = make_float2(1.f / __ldg(a.A + (int64_t)d * N + 2 * p),
+                            1.f / __ldg(a.A + (int64_t)d * N + 2 * p + 1));
+  }
+  const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
+  const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
+
+  float2 h[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
+  if (s0 == 0 && a.h0 != nullptr) {  // NEXT-2: state carried into the row
+    const float* hp = a.h0 + ((int64_t)r * Dn + d) * N;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) h[p] = make_float2(__ldg(hp + 2 * p), __ldg(hp + 2 * p + 1));
+  }
+
+  // Flat loop over 8-step sub-blocks; u/dt of the next sub-block are loaded
+  // into registers before the current one is computed (software pipeline),
+  // B/C/head tiles are restaged at every kTile boundary.  Sub-blocks fully
+  // inside the segment (all but at most two) run without per-step checks.
+  int tb = s0 & ~7;
+  Raw8<T, kVec> pu, pt, pz;
+  pu.load(u_row, tb, L);
+  pt.load(dt_row, tb, L);
+  if (kGate) pz.load(z_row, tb, L);
+  int j0 = -1;
+  unsigned long long hmask = 0ull;
+  for (; tb < s1; tb += 8) {
+    if (j0 < 0 || (tb & (kTile - 1)) == 0) {  // CTA-uniform
+      j0 = tb & ~(kTile - 1);
+      __syncthreads();
+      stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask, a.h0 == nullptr);
+      __syncthreads();
+      // head flags of the tile as a register bitmask (CTA-uniform): no
+      // shared-memory load on the per-step critical path
+      hmask = (unsigned long long)sMask[0] | ((unsigned long long)sMask[1] << 32);
+    }
+    float uu[8], vv[8], yy[8], zz[8];
+    pu.unpack(uu);
+    pt.unpack(vv);
+    if (kGate) pz.unpack(zz);
+    if (tb + 8 < s1) {
+      pu.load(u_row, tb + 8, L);
+      pt.load(dt_row, tb + 8, L);
+      if (kGate) pz.load(z_row, tb + 8, L);
+    }
+    const int sb = tb - j0;
+    // checkpoint = state before step tb (only step i == 0 can be a multiple of kChunk)
+    if (a.states != nullptr && (tb % kChunk) == 0 && tb >= s0 && active) {
+      float* st = a.states + (((int64_t)r * a.nchunk + tb / kChunk) * N) * Dn + d;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        st[(int64_t)(2 * p) * Dn] = h[p].x;
+        st[(int64_t)(2 * p + 1) * Dn] = h[p].y;
+      }
+    }
+    auto block = [&](auto full_tag) {
+      constexpr bool kFull = decltype(full_tag)::value;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int t = tb + i;
+        yy[i] = 0.f;
+        if (!kFull && (t < s0 || t >= s1)) continue;  // CTA-uniform
+        const float v = vv[i] + bias;
+        const float delta = a.softplus ? softplusf(v) : v;
+        const float2 dux2 = f2(delta * uu[i]), dl2 = f2(delta);
+        const float2* Bt = reinterpret_cast<const float2*>(sB[sb + i]);
+        const float2* Ct = reinterpret_cast<const float2*>(sC[sb + i]);
+        if constexpr (kZoh) {  // B-bar u = f(z) delta B u (Eq 2b); abar needed at heads too
+          const bool head = (hmask >> (sb + i)) & 1ull;
+          const float2 u2 = f2(uu[i]);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            const float2 m = fmul2(dl2, A2[p]);
+            const float2 ab = ex2x2(m);
+            const float2 zz2 = fmul2(m, f2(kLn2));
+            const float2 bf = make_float2(zoh_bfac(ab.x, zz2.x, invA[p].x, delta),
+                                          zoh_bfac(ab.y, zz2.y, invA[p].y, delta));
+            const float2 bx = fmul2(bf, fmul2(u2, Bt[p]));
+            h[p] = head ? bx : ffma2(ab, h[p], bx);
+          }
+        } else if ((hmask >> (sb + i)) & 1ull) {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
+        } else {
+#pragma unroll
+          for (int p = 0; p < NP; ++p) h[p] = ffma2(ex2x2(fmul2(dl2, A2[p])), h[p], fmul2(dux2, Bt[p]));
+        }
+        float2 yp[2] = {make_float2(Dd * uu[i], 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int p = 0; p < NP; ++p) yp[p & 1] = ffma2(Ct[p], h[p], yp[p & 1]);
+        const float2 ys = fadd2(yp[0], yp[1]);
+        yy[i] = ys.x + ys.y;
+        if (kGate) yy[i] *= zz[i] * sigmoidf_fast(zz[i]);  // out = y * silu(z)
+      }
+    };
+    if (tb >= s0 && tb + 8 <= s1) block(std::true_type{});
+    else block(std::false_type{});
+    if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
+  }
+  if (s1 == L && a.h_last != nullptr && active) {  // state after the row's last step
+    float* hp = a.h_last + ((int64_t)r * Dn + d) * N;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      hp[2 * p] = h[p].x;
+      hp[2 * p + 1] = h[p].y;
+    }
+  }
+  }  // work loop
+}
+
+// ===========================================================================
+// host side
+// ===========================================================================
+namespace {
+
+// persistent grid: resident CTAs on all SMs, capped by the number of items
+template <typename K>
+int persistent_grid(K kern, int threads, size_t smem, int64_t items) {
+  int dev = 0, nsm = 148, nb = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
+  const int64_t g = (int64_t)nsm * std::max(nb, 1);
+  if (getenv("PM_DEBUG"))
+    fprintf(stderr, "[pm] persistent grid: nsm=%d blocks/SM=%d (err=%d) smem=%zu items=%lld -> %lld\n",
+            nsm, nb, (int)e, smem, (long long)items, (long long)std::min<int64_t>(g, items));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, items));
+}
+
+template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh>
+void fwd_go(const ScanFwdArgs& a, cudaStream_t s) {
+  auto kern = scan_fwd_kernel<T, N, kVec, MinB, kGate, kZoh>;
+  if (a.items != nullptr) {
+    const int g = persistent_grid(kern, kScanThreads, 0, (int64_t)a.n_items * n_dblk(a.Dn));
+    kern<<<g, kScanThreads, 0, s>>>(a);
+  } else {
+    kern<<<dim3(n_dblk(a.Dn), a.R, a.nseg), kScanThreads, 0, s>>>(a);
+  }
+}
+
+template <typename T, int N, bool kVec>
+pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
+  if (a.items != nullptr) {  // schedule: plan + sort (reads pos only), reset counter
+    Sched sc = sched_of(a.states, a.R, a.Dn, a.L, N);
+    if (cudaMemsetAsync(sc.counters, 0, 256, s) != cudaSuccess) return PM_ERR_CUDA;
+    seg_plan_kernel<<<a.R, 256, 0, s>>>(a.pos, a.L, a.nseg, sc.unsorted);
+    PM_LAUNCH_CHECK();
+    seg_sort_kernel<<<1, 1024, 0, s>>>(sc.unsorted, a.n_items, a.L, sc.sorted);
+    PM_LAUNCH_CHECK();
+  }
+  if (a.zoh) {
+    // ZOH carries 1/A and the series: 3 CTAs/SM (168 registers) avoid spills
+    if (a.z != nullptr) fwd_go<T, N, kVec, 3, true, true>(a, s);
+    else fwd_go<T, N, kVec, 3, false, true>(a, s);
+  } else {
+    if (a.z != nullptr) fwd_go<T, N, kVec, kFwdMinB, true, false>(a, s);
+    else fwd_go<T, N, kVec, kFwdMinB, false, false>(a, s);
+  }
+  PM_LAUNCH_CHECK();
+  return PM_OK;
+}
+
+template <typename T, int N>
+pm_status dispatch_fwd_vec(const ScanFwdArgs& a, bool vec, cudaStream_t s) {
+  return vec ? launch_fwd<T, N, true>(a, s) : launch_fwd<T, N, false>(a, s);
+}
+
+template <typename T>
+pm_status dispatch_fwd_t(const ScanFwdArgs& a, int N, bool vec, cudaStream_t s) {
+  switch (N) {
+    case 4: return dispatch_fwd_vec<T, 4>(a, vec, s);
+    case 8: return dispatch_fwd_vec<T, 8>(a, vec, s);
+    default: return dispatch_fwd_vec<T, 16>(a, vec, s);
+  }
+}
+
+}  // namespace
+
+pm_status run_scan_fwd(const ScanFwdArgs& a, int N, bool vec, pm_dtype io, cudaStream_t s) {
+  return io == PM_F32 ? dispatch_fwd_t<float>(a, N, vec, s) : dispatch_fwd_t<__nv_bfloat16>(a, N, vec, s);
+}
+
+}  // namespace pm

@@ -1,0 +1,188 @@
+// scan_impl.cuh -- shared declarations of the ScanOp_pack kernels (Alg 2
+// P:172-185, Eq 1a/1b/2a P:202-205, sec 3.4 P:199-224 of arXiv 2408.03865).
+//
+// Design:
+//  * forward: one thread = one (row, channel) lane holding all N states in
+//    registers, sequential in time; a CTA = 128 consecutive channels of one
+//    row, so the head predicate is CTA-uniform (no divergence) and B/C/pos
+//    tiles are staged once in shared memory (fp32) and broadcast;
+//  * time parallelism comes from the packing itself: a row is split at
+//    sequence heads into independent segments (sequences never span
+//    rows, and the reset cuts every carry), so no carry fix-up and no
+//    redundant exponentials are needed; segments are scheduled
+//    longest-first on persistent CTAs;
+//  * the reset is a select on the CTA-uniform head flag (h = b), never a
+//    multiply by 0, so NaN/Inf and -0 cannot cross a boundary;
+//  * forward saves the state every kChunk steps ("reused Mamba's structure
+//    for handling hidden_state"); backward walks chunks in reverse,
+//    parks every step's state of the chunk in TMEM, runs the reverse
+//    recurrence g_t = C_t dy_t + abar_{t+1} g_{t+1} (abar = 0 at heads,
+//    P:224) and reduces dB/dC over channels with a warp transpose through
+//    shared memory, then over warps, into per-channel-block partials that a
+//    finalize kernel sums in a fixed order (deterministic).
+//  * scan_fwd.cu holds the forward + schedule kernels, scan_bwd.cu the
+//    backward, scan.cu the C ABI (validation, workspace layout).
+#pragma once
+#include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace pm {
+
+constexpr int kScanThreads = 128;
+constexpr int kScanWarps = kScanThreads / 32;
+constexpr int kTile = 64;   // fwd staging tile (time steps)
+constexpr int kChunk = 16;  // checkpoint interval (time steps)
+constexpr int kFwdMinB = 4;  // resident fwd CTAs per SM (register cap 128)
+constexpr int kBwdMinB = 4;  // resident bwd CTAs per SM (register cap 128; smem fits 4)
+
+constexpr int kBwdCh = 64;                   // channels per CTA
+constexpr int kBwdThreads = 2 * kBwdCh;      // lane pair per channel
+constexpr int kBwdWarps = kBwdThreads / 32;
+constexpr int kRedStride = 32;               // float4 per transpose row (no padding)
+constexpr int kBSub = 2;                     // bwd register sub-chunk (= one reduction round)
+constexpr int kBNSub = kChunk / kBSub;
+static_assert(kChunk == 16, "phase 1 maps 8 steps to each thread of a pair");
+
+struct ScanFwdArgs {
+  const void* u;
+  const void* dt;
+  const float* A;
+  const void* B;
+  const void* C;
+  const float* Dskip;
+  const float* dt_bias;
+  const int32_t* pos;
+  void* y;
+  float* states;
+  const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
+  int* counter;       // work counter for the persistent loop
+  int n_items;
+  int R, Dn, L, nseg, nchunk, softplus;
+  const void* z;      // NEXT-1 gate (R,Dn,L) or NULL: y <- y * silu(z)
+  const float* h0;    // NEXT-2 state entering t=0 (R,Dn,N) or NULL
+  float* h_last;      // state after step L-1 (R,Dn,N) or NULL
+  int zoh;             // NEXT-4: Eq 2b discretisation of B-bar (else Euler, Q1)
+};
+
+struct ScanBwdArgs {
+  const void* u;
+  const void* dt;
+  const float* A;
+  const void* B;
+  const void* C;
+  const float* Dskip;
+  const float* dt_bias;
+  const int32_t* pos;
+  const float* states;
+  const void* dy;
+  void* du;
+  void* ddt;
+  float* ws_bc;     // (nDblk, R, L, 2N)
+  float* ws_param;  // (R*nseg, N+2, Dn)
+  const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
+  int* counter;
+  int n_items;
+  int R, Dn, L, nseg, nchunk, softplus;
+  const void* z;        // NEXT-1 gate (R,Dn,L) or NULL; dy is then d(out)
+  const float* h0;      // NEXT-2 state entering t=0 (R,Dn,N) or NULL
+  const float* dh_last; // cotangent of the state after step L-1 or NULL
+  void* dz;             // (R,Dn,L) when z != NULL
+  float* dh0;           // (R,Dn,N) when h0 != NULL
+  int zoh;              // NEXT-4: Eq 2b discretisation of B-bar (else Euler, Q1)
+};
+
+// ---------------------------------------------------------------------------
+// Stage B, C (converted to fp32, time-major [t][n]) and head flags for the
+// time window [j0, j0 + W) of row r into shared memory.
+template <typename T, int N, int W, bool kVec>
+PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
+                     const int32_t* __restrict__ pos_row, int L, int j0,
+                     float (*sB)[N], float (*sC)[N], unsigned* sMask, bool t0_head) {
+  static_assert(W % 8 == 0, "window must be a multiple of 8");
+  for (int e = threadIdx.x; e < N * (W / 8); e += blockDim.x) {
+    const int n = e % N, tb = (e / N) * 8;
+    float vb[8], vc[8];
+    load8<T, kVec>(B_r + (int64_t)n * L, j0 + tb, L, vb);
+    load8<T, kVec>(C_r + (int64_t)n * L, j0 + tb, L, vc);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      sB[tb + i][n] = vb[i];
+      sC[tb + i][n] = vc[i];
+    }
+  }
+  // head flags of the window as a bitmask (warp 0 ballots 32 steps at a time)
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int w0 = 0; w0 < W; w0 += 32) {
+      const int t = j0 + w0 + (int)threadIdx.x;
+      const bool f = (w0 + (int)threadIdx.x < W) &&
+                     ((t >= L) || (t == 0 && t0_head) || __ldg(pos_row + t) == 0);
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (threadIdx.x == 0) sMask[w0 / 32] = m;
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// host-side helpers shared by the three translation units
+// ---------------------------------------------------------------------------
+inline int n_chunks(int64_t L) { return (int)((L + kChunk - 1) / kChunk); }
+inline int n_dblk(int64_t Dn) { return (int)((Dn + kScanThreads - 1) / kScanThreads); }
+inline int n_dblk_bwd(int64_t Dn) { return (int)((Dn + kBwdCh - 1) / kBwdCh); }
+
+// Segments per row: nominal cut every 256 steps (cuts snap to heads, so with
+// the paper's length distribution a segment is ~one sequence), <= 64.
+inline int n_seg(int64_t L) { return (int)std::max<int64_t>(1, std::min<int64_t>(64, L / 256)); }
+
+// states buffer = fp32 chunk states | 256 B counters | sorted segment list |
+// unsorted segment list (the fwd writes the schedule; the bwd reuses it)
+inline size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
+inline size_t states_f32_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  return (size_t)R * n_chunks(L) * N * Dn * sizeof(float);
+}
+inline size_t sched_bytes(int64_t R, int64_t L) { return 256 + 2 * up256((size_t)R * n_seg(L) * 16); }
+inline size_t state_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  return up256(states_f32_bytes(R, Dn, L, N)) + sched_bytes(R, L);
+}
+struct Sched {
+  int* counters;
+  int4* sorted;
+  int4* unsorted;
+};
+inline Sched sched_of(void* states, int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  char* b = static_cast<char*>(states) + up256(states_f32_bytes(R, Dn, L, N));
+  Sched sc;
+  sc.counters = reinterpret_cast<int*>(b);
+  sc.sorted = reinterpret_cast<int4*>(b + 256);
+  sc.unsorted = reinterpret_cast<int4*>(b + 256 + up256((size_t)R * n_seg(L) * 16));
+  return sc;
+}
+
+inline bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+inline pm_status check_common(int64_t R, int64_t Dn, int64_t L, int32_t N, pm_dtype io) {
+  if (R < 1 || Dn < 1 || L < 1) return PM_ERR_INVALID_ARG;
+  if (io != PM_F32 && io != PM_BF16) return PM_ERR_DTYPE;
+  if (N != 4 && N != 8 && N != 16) return PM_ERR_UNSUPPORTED;
+  if (R * L >= (int64_t(1) << 31) || Dn >= (int64_t(1) << 31)) return PM_ERR_SHAPE;
+  if (R > 65535 || R * n_seg(L) * ((Dn + kBwdCh - 1) / kBwdCh) >= (int64_t(1) << 31)) return PM_ERR_SHAPE;
+  return PM_OK;
+}
+
+inline bool elem_aligned(const void* p, pm_dtype io) {
+  const uintptr_t m = io == PM_F32 ? 3u : 1u;
+  return p == nullptr || (reinterpret_cast<uintptr_t>(p) & m) == 0;
+}
+
+
+// launchers (scan_fwd.cu / scan_bwd.cu)
+pm_status run_scan_fwd(const ScanFwdArgs& a, int N, bool vec, pm_dtype io, cudaStream_t s);
+pm_status run_scan_bwd(const ScanBwdArgs& a, int N, bool vec, pm_dtype io, float* dA, float* dB,
+                       float* dC, float* dD, float* ddtb, cudaStream_t s);
+
+}  // namespace pm

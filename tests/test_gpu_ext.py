@@ -39,24 +39,25 @@ def problem(R, Dn, L, N, kind, io, seed, continued=(), dev="cuda"):
     return pos, u, T, P, z, h0, dh
 
 
-def run_ext(pos, u, T, P, z, h0, dh, states=True):
+def run_ext(pos, u, T, P, z, h0, dh, states=True, zoh=False):
     out, st, hl = pm.pm_selective_scan_fwd_ex(u, T["dt"], P["A"], T["B"], T["C"], P["D"],
                                                P["dt_bias"], pos, z=z, h0=h0,
-                                               want_states=states, want_last_state=True)
+                                               want_states=states, want_last_state=True,
+                                               zoh=zoh)
     g = pm.pm_selective_scan_bwd_ex(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
                                     pos, T["dy"], z=z, h0=h0, states=st, dh_last=dh,
-                                    want_dh0=True)
+                                    want_dh0=True, zoh=zoh)
     torch.cuda.synchronize()
     return out, hl, g
 
 
-def check_ext(pos, u, T, P, z, h0, dh, io, res):
+def check_ext(pos, u, T, P, z, h0, dh, io, res, zoh=False):
     out, hl, g = res
     args = (to_np(u), to_np(T["dt"]), to_np(P["A"]), to_np(T["B"]), to_np(T["C"]),
             to_np(P["D"]), to_np(P["dt_bias"]), to_np(pos).astype(np.int32))
     zz, hh = to_np(z), to_np(h0)
-    ro, rhl = oracle.scan_fwd_ext(*args, z=zz, h0=hh)
-    ref = oracle.scan_bwd_ext(*args, to_np(T["dy"]), z=zz, h0=hh, dh_last=to_np(dh))
+    ro, rhl = oracle.scan_fwd_ext(*args, z=zz, h0=hh, zoh=zoh)
+    ref = oracle.scan_bwd_ext(*args, to_np(T["dy"]), z=zz, h0=hh, dh_last=to_np(dh), zoh=zoh)
     errs = {"out": (rel_err(to_np(out), ro), "fwd"), "h_last": (rel_err(to_np(hl), rhl), "fwd")}
     for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dz", "dh0"):
         if ref.get(k) is not None and g.get(k) is not None:
@@ -147,3 +148,37 @@ def test_cut_row_state_passing_reproduces_uncut(m):
         assert torch.equal(torch.cat([g1[k], g2[k]], -1), full[2][k]), k
     for k in ("dA", "dD", "ddt_bias"):
         torch.testing.assert_close(g1[k] + g2[k], full[2][k], rtol=1e-5, atol=1e-5)
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: ZOH discretisation (Eq 2b)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+@pytest.mark.parametrize("gate", [False, True])
+def test_zoh_parity(io, gate):
+    """delta in [1e-3, 0.1+] and A in [-17, -1] put z = delta A on both sides
+    of the series / closed-form switch at |z| = 0.1."""
+    pos, u, T, P, z, h0, dh = problem(3, 200, 1024, 16, "random", io, seed=70 + gate,
+                                      continued=(1,))
+    z = z if gate else None
+    check_ext(pos, u, T, P, z, h0, dh, io, run_ext(pos, u, T, P, z, h0, dh, zoh=True), zoh=True)
+
+
+@pytest.mark.parametrize("N,L", [(4, 13), (8, 700)])
+def test_zoh_shapes_and_zero_A(N, L):
+    """Scalar path, other N, and a zero column of A (f(0) = 1: the series)."""
+    pos, u, T, P, z, h0, dh = problem(2, 70, L, N, "random", "f32", seed=80 + N, continued=(0,))
+    P["A"][3] = 0.0
+    P["A"][5, 1] = -1e-6
+    check_ext(pos, u, T, P, None, h0, dh, "f32", run_ext(pos, u, T, P, None, h0, dh, zoh=True),
+              zoh=True)
+
+
+def test_zoh_recompute_equals_saved():
+    pos, u, T, P, z, h0, dh = problem(2, 96, 900, 16, "edges", "f32", seed=90, continued=(1,))
+    a = run_ext(pos, u, T, P, z, h0, dh, states=True, zoh=True)
+    b = run_ext(pos, u, T, P, z, h0, dh, states=False, zoh=True)
+    assert torch.equal(a[0], b[0])
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dz", "dh0"):
+        assert torch.equal(a[2][k], b[2][k]), k
