@@ -205,6 +205,26 @@ PM_DEV void store2(T* __restrict__ p, int64_t i, int64_t lo, int64_t hi, const f
   }
 }
 
+// 8 consecutive elements from 16-byte aligned shared memory, as fp32
+template <typename T>
+PM_DEV void smem_load8(const T* p, float (&v)[8]) {
+  if constexpr (sizeof(T) == 2) {
+    const uint4 q = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 f = __bfloat1622float2(b[k]);
+      v[2 * k] = f.x;
+      v[2 * k + 1] = f.y;
+    }
+  } else {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+
 template <typename T, bool kVec>
 struct Raw8 {  // 8 consecutive I/O elements held raw in registers (prefetch)
   float v[8];

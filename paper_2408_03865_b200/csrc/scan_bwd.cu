@@ -219,16 +219,10 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     {
       float uu[8], vv[8], yy[8], zz[8];
       if constexpr (kVec) {
-        const T* ru = &sm.raw.u[cl][8 * hf];
-        const T* rt = &sm.raw.dt[cl][8 * hf];
-        const T* ry = &sm.raw.dy[cl][8 * hf];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          uu[i] = IO<T>::cvt(ru[i]);
-          vv[i] = IO<T>::cvt(rt[i]);
-          yy[i] = IO<T>::cvt(ry[i]);
-          if constexpr (kGate) zz[i] = IO<T>::cvt(sm.raw.z[cl][8 * hf + i]);
-        }
+        smem_load8<T>(&sm.raw.u[cl][8 * hf], uu);
+        smem_load8<T>(&sm.raw.dt[cl][8 * hf], vv);
+        smem_load8<T>(&sm.raw.dy[cl][8 * hf], yy);
+        if constexpr (kGate) smem_load8<T>(&sm.raw.z[cl][8 * hf], zz);
       } else {
         load8<T, false>(u_row, cb + 8 * hf, L, uu);
         load8<T, false>(dt_row, cb + 8 * hf, L, vv);
