@@ -175,8 +175,6 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   const T* u_row = static_cast<const T*>(a.u) + lane;
   const T* dt_row = static_cast<const T*>(a.dt) + lane;
   const T* dy_row = static_cast<const T*>(a.dy) + lane;
-  T* du_row = static_cast<T*>(a.du) + lane;
-  T* ddt_row = static_cast<T*>(a.ddt) + lane;
   float* ws_bc_r = a.ws_bc + ((int64_t)dblk * a.R + r) * (int64_t)L * (2 * N);
 
   // a thread's NH states are processed in pairs with packed fp32x2 (FFMA2)
@@ -208,7 +206,6 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     for (int p = 0; p < NP; ++p) g[p] = make_float2(__ldg(gp + 2 * p), __ldg(gp + 2 * p + 1));
   }
   const T* z_row = kGate ? static_cast<const T*>(a.z) + lane : nullptr;
-  T* dz_row = kGate ? static_cast<T*>(a.dz) + lane : nullptr;
 
   for (int c = clast; c >= cfirst; --c) {
     const int cb = c * kChunk, c0 = max(cb, s0), c1 = min(cb + kChunk, s1);
@@ -474,16 +471,12 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         if (row < kRows && ch == 0) sm.xw[sc][wid][row][rh] = acc;
       }
       __syncwarp();
-      if (active && hf == 0) {
-        if (kFull) {
-          store2<T, kVec>(du_row, a0, a0, a0 + kBSub, duo);
-          store2<T, kVec>(ddt_row, a0, a0, a0 + kBSub, ddo);
-          if constexpr (kGate) store2<T, kVec>(dz_row, a0, a0, a0 + kBSub, dzo);
-        } else {
-          store2<T, kVec>(du_row, a0, c0, c1, duo);
-          store2<T, kVec>(ddt_row, a0, c0, c1, ddo);
-          if constexpr (kGate) store2<T, kVec>(dz_row, a0, c0, c1, dzo);
-        }
+      // the step's scalars are consumed: park (du, ddt, dz) in their slot;
+      // the chunk's rows are written to HBM with full-sector stores below
+      if (hf == 0) {
+#pragma unroll
+        for (int i = 0; i < kBSub; ++i)
+          sm.sc[a0 - cb + i][cl] = make_float4(duo[i], ddo[i], dzo[i], 0.f);
       }
     };
     if constexpr (kFull) {
@@ -515,6 +508,28 @@ scan_bwd_kernel(const ScanBwdArgs a) {
           for (int w = 0; w < kBwdWarps; ++w) acc += p[w * kWStride];
           ws_bc_r[(int64_t)t * (2 * N) + v] = acc;
         }
+      }
+    }
+    // ---- du / ddt (/ dz) rows of the chunk: thread pair (2c, 2c+1) writes
+    //      channel c's du and ddt, 16 contiguous steps each ----
+    {
+      constexpr int kArr = kGate ? 3 : 2;
+      for (int e = tid; e < kArr * kBwdCh; e += kBwdThreads) {
+        const int cc = e < 2 * kBwdCh ? e >> 1 : e - 2 * kBwdCh;
+        const int which = e < 2 * kBwdCh ? (e & 1) : 2;
+        const int dd = dblk * kBwdCh + cc;
+        if (dd >= Dn) continue;
+        T* dst = static_cast<T*>(which == 0 ? a.du : which == 1 ? a.ddt : a.dz) +
+                 ((int64_t)r * Dn + dd) * L;
+        static_assert(kChunk == 16, "two 8-element vectors per row");
+        float v[2][8];
+#pragma unroll
+        for (int ii = 0; ii < kChunk; ++ii) {
+          const float4 q = sm.sc[ii][cc];
+          v[ii >> 3][ii & 7] = which == 0 ? q.x : which == 1 ? q.y : q.z;
+        }
+        store8<T, kVec>(dst, cb, c0, c1, v[0]);
+        store8<T, kVec>(dst, cb + 8, c0, c1, v[1]);
       }
     }
   }
