@@ -11,22 +11,23 @@ namespace pm {
 // Layout: a CTA owns kBwdCh channels of one row and one time segment; each
 // channel is served by a lane pair (lane = 2*c + hf), thread hf holding the
 // NH = N/2 states [hf*NH, hf*NH + NH) -- half the registers of a
-// one-thread-per-channel design, so 12 warps fit per SM.
+// one-thread-per-channel design, so 4 CTAs (16 warps) fit per SM.
 // Per chunk of kChunk steps (walked in reverse):
 //   staging: every per-chunk input (u, dt, dy rows, B, C, pos, the saved
 //            chunk state) is fetched with cp.async one chunk AHEAD into a raw
 //            shared buffer, so no global latency sits on the critical path;
 //   phase 1: per-(t,d) scalars delta, u, dy, softplus'(v) computed once into
 //            shared memory; B/C converted to fp32; head flags;
-//   pass A : forward recompute from the saved chunk state, storing the state
-//            at every kSub-step sub-chunk start (shared memory);
-//   pass B : per sub-chunk (reverse): recompute h_t, abar_t into registers,
-//            then the reverse recurrence g_t = C_t dy_t + abar_{t+1} g_{t+1}
-//            (abar = 0 at heads); sum_n terms are combined across the
-//            lane pair with one shuffle; dB/dC values are reduced over each
-//            warp's channels in 2-step rounds (warp transpose through a
-//            conflict-free padded buffer) and the per-warp partials of the
-//            whole chunk are summed across warps after ONE barrier.
+//   pass A : forward recompute from the saved chunk state, parking the state
+//            entering every step in TMEM;
+//   pass B : 2-step rounds in reverse: h_{t-1}, h_t come back from TMEM and
+//            the reverse recurrence g_t = C_t dy_t + abar_{t+1} g_{t+1}
+//            (abar = 0 at heads) runs in registers; sum_n terms are
+//            combined across the lane pair with one shuffle; dB/dC values
+//            are reduced over each warp's channels per round (warp transpose
+//            through shared memory); the per-warp partials of the whole
+//            chunk are summed across warps after ONE barrier, and the
+//            chunk's du/ddt rows leave with full-sector vector stores.
 
 template <typename T, int N, bool kGate>
 struct BwdRaw {  // raw inputs of one chunk, filled by cp.async (vector path)
