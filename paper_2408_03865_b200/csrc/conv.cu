@@ -200,11 +200,20 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
   const int nblk = (te - tb + kSpan - 1) / kSpan;
   Raw8<T, kVec> nx, ng;
   Pos8<kVec> np;
+  // left halo of x for lane 0 (x[t0-K+1 .. t0-1]), loaded one iteration
+  // ahead so no dependent global load sits in the loop body
+  float hx[H];
+  auto load_halo = [&](int t0l) {
+#pragma unroll
+    for (int o = 1; o < K; ++o)
+      hx[o - 1] = (lid == 0 && t0l - o >= 0) ? IO<T>::ld(xr + t0l - o) : 0.f;
+  };
   {
     const int t0 = tb + (nblk - 1) * kSpan + lid * kCE;
     nx.load(xr, t0, te);
     ng.load(gr, t0, te);
     np.load(prow, t0, te);
+    load_halo(tb + (nblk - 1) * kSpan);
   }
   for (int blk = nblk - 1; blk >= 0; --blk) {
     const int t0 = tb + blk * kSpan + lid * kCE;
@@ -214,17 +223,18 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
     ng.unpack(gv);
 #pragma unroll
     for (int i = 0; i < 8; ++i) p[i] = np.p[i];
-    if (blk > 0) {  // prefetch the earlier block
-      nx.load(xr, t0 - kSpan, te);
-      ng.load(gr, t0 - kSpan, te);
-      np.load(prow, t0 - kSpan, te);
-    }
-    // left halo of x: lane-1 (lane 0 reads the earlier block directly)
+    // left halo of x: lane-1 (lane 0: the value prefetched last iteration)
     float X[K - 1 + 8];
 #pragma unroll
     for (int o = 1; o < K; ++o) {
       const float v = __shfl_up_sync(0xffffffffu, xv[8 - o], 1);
-      X[K - 1 - o] = lid == 0 ? ((t0 - o >= 0) ? IO<T>::ld(xr + t0 - o) : 0.f) : v;
+      X[K - 1 - o] = lid == 0 ? hx[o - 1] : v;
+    }
+    if (blk > 0) {  // prefetch the earlier block and its halo
+      nx.load(xr, t0 - kSpan, te);
+      ng.load(gr, t0 - kSpan, te);
+      np.load(prow, t0 - kSpan, te);
+      load_halo(tb + (blk - 1) * kSpan);
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) X[K - 1 + i] = xv[i];
@@ -243,9 +253,27 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
 #pragma unroll
     for (int o = 1; o < K; ++o) full = full && ph[o - 1] >= K - 1;
     const bool wfull = __all_sync(0xffffffffu, full);
+    // every slot of the window (and of its right halo) a head -- e.g. the
+    // padding run at the end of a row: only the o = 0 tap survives
+    bool heads = t0 + 8 <= te;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) heads = heads && p[i] == 0;
+#pragma unroll
+    for (int o = 1; o < K; ++o) heads = heads && ph[o - 1] == 0;
+    const bool wheads = K > 1 && !wfull && __all_sync(0xffffffffu, heads);
     float dp[8 + H];
     float dxv[8];
-    if (wfull) {
+    if (wheads) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float pre = fmaf(wk[K - 1], xv[i], b);
+        const float dpv = gv[i] * (kSilu ? silu_grad(pre) : 1.f);
+        dp[i] = dpv;
+        acc_b += dpv;
+        acc_w[K - 1] = fmaf(dpv, xv[i], acc_w[K - 1]);
+        dxv[i] = wk[K - 1] * dpv;
+      }
+    } else if (wfull) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float pre = b;
@@ -273,20 +301,17 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int t = t0 + i;
+        const int ci = min(p[i], t);  // tap o is kept iff o <= pos[t] and t - o >= 0
         float pre = b;
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int o = K - 1 - j;
-          if (o <= p[i] && t - o >= 0) pre = fmaf(wk[j], X[i + j], pre);
-        }
+        for (int j = 0; j < K; ++j)
+          if (K - 1 - j <= ci) pre = fmaf(wk[j], X[i + j], pre);
         const float dpv = (t < te) ? gv[i] * (kSilu ? silu_grad(pre) : 1.f) : 0.f;
         dp[i] = dpv;
         acc_b += dpv;
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int o = K - 1 - j;
-          if (o <= p[i] && t - o >= 0) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
-        }
+        for (int j = 0; j < K; ++j)
+          if (K - 1 - j <= ci) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
       }
 #pragma unroll
       for (int o = 1; o < K; ++o) {
@@ -298,9 +323,9 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
         float a = 0.f;
 #pragma unroll
         for (int o = 0; o < K; ++o) {
-          const int t = t0 + i + o;
+          // dp is 0 at and beyond L (own block: t >= te; carry: 0 past L)
           const int pt = (i + o < 8) ? p[i + o] : ph[i + o - 8];
-          if (t < L && o <= pt) a = fmaf(wk[K - 1 - o], dp[i + o], a);
+          if (o <= pt) a = fmaf(wk[K - 1 - o], dp[i + o], a);
         }
         dxv[i] = a;
       }
