@@ -572,11 +572,19 @@ scan_bwd_finalize_bc(const float* __restrict__ ws_bc, float* __restrict__ dB,
   const int r = blockIdx.y, t0 = blockIdx.x * TT;
   for (int e = threadIdx.x; e < TT * 2 * N; e += blockDim.x) {
     const int tt = e / (2 * N), v = e % (2 * N), t = t0 + tt;
-    float s = 0.f;
-    if (t < L)
-      for (int b = 0; b < nblk; ++b)
-        s += ws_bc[(((int64_t)b * R + r) * L + t) * (2 * N) + v];
-    tile[v][tt] = s;
+    // 8 independent partial sums (loads in flight), combined in a fixed order
+    float p[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (t < L) {
+      const float* src = ws_bc + ((int64_t)r * L + t) * (2 * N) + v;
+      const int64_t stride = (int64_t)R * L * (2 * N);
+      int b = 0;
+      for (; b + 8 <= nblk; b += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) p[k] += __ldcs(src + (b + k) * stride);
+      }
+      for (; b < nblk; ++b) p[b & 7] += __ldcs(src + b * stride);
+    }
+    tile[v][tt] = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
   }
   __syncthreads();
   for (int e = threadIdx.x; e < TT * 2 * N; e += blockDim.x) {
@@ -596,8 +604,17 @@ scan_bwd_finalize_param(const float* __restrict__ ws, float* __restrict__ dA,
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)(N + 2) * Dn) return;
   const int n = (int)(e / Dn), d = (int)(e % Dn);
-  float s = 0.f;
-  for (int i = 0; i < nrs; ++i) s += ws[((int64_t)i * (N + 2) + n) * Dn + d];
+  // 8 independent partial sums (loads in flight), combined in a fixed order
+  float p[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  const float* src = ws + (int64_t)n * Dn + d;
+  const int64_t stride = (int64_t)(N + 2) * Dn;
+  int i = 0;
+  for (; i + 8 <= nrs; i += 8) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p[k] += __ldcs(src + (i + k) * stride);
+  }
+  for (; i < nrs; ++i) p[i & 7] += __ldcs(src + i * stride);
+  const float s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
   if (n < N) dA[(int64_t)d * N + n] = s;
   else if (n == N) { if (dD) dD[d] = s; }
   else { if (ddtb) ddtb[d] = s; }

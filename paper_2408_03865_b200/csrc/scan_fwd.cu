@@ -20,11 +20,18 @@ __global__ void __launch_bounds__(256) seg_plan_kernel(const int32_t* __restrict
   const int seg = (L + nseg - 1) / nseg;
   for (int k = 1 + warp; k < nseg; k += blockDim.x >> 5) {
     int b = L;
-    for (int base = k * seg; base < L; base += 32) {
-      const int t = base + lane;
-      const unsigned m = __ballot_sync(0xffffffffu, t < L && __ldg(pos_row + t) == 0);
+    // 128 positions per ballot round (4 per lane), one load round trip each
+    for (int base = k * seg; base < L; base += 128) {
+      int f = 4;  // first head among my 4 positions (4 = none)
+#pragma unroll
+      for (int q = 3; q >= 0; --q) {
+        const int t = base + 4 * lane + q;
+        if (t < L && __ldg(pos_row + t) == 0) f = q;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, f < 4);
       if (m) {
-        b = base + __ffs(m) - 1;
+        const int src = __ffs(m) - 1;
+        b = base + 4 * src + __shfl_sync(0xffffffffu, f, src);
         break;
       }
     }
