@@ -108,9 +108,18 @@ conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
     for (int i = 0; i < 8; ++i) X[K - 1 + i] = xv[i];
 #pragma unroll
     for (int o = 1; o < K; ++o) carry[o - 1] = __shfl_sync(0xffffffffu, xv[8 - o], 31);
-    bool full = t0 >= K - 1 || t0 >= te;
+    // one decision per iteration: all 8 steps inside [tb, te) with every tap
+    // in range (the common case), all 8 steps sequence heads (e.g. padding),
+    // else per-step tap masks
+    int pmin = p[0], pmax = p[0];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) full = full && (p[i] >= K - 1 || t0 + i >= te);
+    for (int i = 1; i < 8; ++i) {
+      pmin = min(pmin, p[i]);
+      pmax = max(pmax, p[i]);
+    }
+    const bool inr = t0 + 8 <= te;
+    const bool full = inr && t0 >= K - 1 && pmin >= K - 1;
+    const bool heads = inr && pmax == 0 && pmin == 0;
     float yv[8];
     if (__all_sync(0xffffffffu, full)) {
 #pragma unroll
@@ -120,15 +129,20 @@ conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
         for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
         yv[i] = kSilu ? pre * sigmoidf_fast(pre) : pre;
       }
+    } else if (__all_sync(0xffffffffu, heads)) {  // only the o = 0 tap survives
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float pre = fmaf(wk[K - 1], xv[i], b);
+        yv[i] = kSilu ? pre * sigmoidf_fast(pre) : pre;
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
+        const int ci = min(p[i], t0 + i);  // tap o kept iff o <= pos[t] and t - o >= 0
         float pre = b;
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const int o = K - 1 - j;
-          if (o <= p[i] && t0 + i - o >= 0) pre = fmaf(wk[j], X[i + j], pre);
-        }
+        for (int j = 0; j < K; ++j)
+          if (K - 1 - j <= ci) pre = fmaf(wk[j], X[i + j], pre);
         yv[i] = kSilu ? pre * sigmoidf_fast(pre) : pre;
       }
     }
@@ -247,19 +261,23 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
     }
     // one decision per iteration: every forward tap and every dx tap valid,
     // all 8 steps inside the range (the common case), else per-tap predicates
-    bool full = t0 >= K - 1 && t0 + 8 <= te && t0 + 8 + K - 2 < L;
+    int pmin = p[0], pmax = p[0];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) full = full && p[i] >= K - 1;
+    for (int i = 1; i < 8; ++i) {
+      pmin = min(pmin, p[i]);
+      pmax = max(pmax, p[i]);
+    }
 #pragma unroll
-    for (int o = 1; o < K; ++o) full = full && ph[o - 1] >= K - 1;
+    for (int o = 1; o < K; ++o) {
+      pmin = min(pmin, ph[o - 1]);
+      pmax = max(pmax, ph[o - 1]);
+    }
+    const bool inr = t0 + 8 <= te;
+    const bool full = inr && t0 >= K - 1 && t0 + 8 + K - 2 < L && pmin >= K - 1;
     const bool wfull = __all_sync(0xffffffffu, full);
     // every slot of the window (and of its right halo) a head -- e.g. the
     // padding run at the end of a row: only the o = 0 tap survives
-    bool heads = t0 + 8 <= te;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) heads = heads && p[i] == 0;
-#pragma unroll
-    for (int o = 1; o < K; ++o) heads = heads && ph[o - 1] == 0;
+    const bool heads = inr && pmax == 0 && pmin == 0;
     const bool wheads = K > 1 && !wfull && __all_sync(0xffffffffu, heads);
     float dp[8 + H];
     float dxv[8];
