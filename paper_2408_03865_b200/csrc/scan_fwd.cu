@@ -204,8 +204,11 @@ scan_fwd_kernel(const ScanFwdArgs a) {
         st[(int64_t)(2 * p + 1) * Dn] = h[p].y;
       }
     }
-    auto block = [&](auto full_tag) {
+    // kFull: all 8 steps inside the segment; kNoHead: and none is a head
+    // (most blocks) -- no per-step check at all
+    auto block = [&](auto full_tag, auto nohead_tag) {
       constexpr bool kFull = decltype(full_tag)::value;
+      constexpr bool kNoHead = decltype(nohead_tag)::value;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int t = tb + i;
@@ -217,7 +220,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
         const float2* Bt = reinterpret_cast<const float2*>(sB[sb + i]);
         const float2* Ct = reinterpret_cast<const float2*>(sC[sb + i]);
         if constexpr (kZoh) {  // B-bar u = f(z) delta B u (Eq 2b); abar needed at heads too
-          const bool head = (hmask >> (sb + i)) & 1ull;
+          const bool head = !kNoHead && ((hmask >> (sb + i)) & 1ull);
           const float2 u2 = f2(uu[i]);
 #pragma unroll
           for (int p = 0; p < NP; ++p) {
@@ -229,7 +232,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
             const float2 bx = fmul2(bf, fmul2(u2, Bt[p]));
             h[p] = head ? bx : ffma2(ab, h[p], bx);
           }
-        } else if ((hmask >> (sb + i)) & 1ull) {
+        } else if (!kNoHead && ((hmask >> (sb + i)) & 1ull)) {
 #pragma unroll
           for (int p = 0; p < NP; ++p) h[p] = fmul2(dux2, Bt[p]);
         } else {
@@ -244,8 +247,12 @@ scan_fwd_kernel(const ScanFwdArgs a) {
         if (kGate) yy[i] *= zz[i] * sigmoidf_fast(zz[i]);  // out = y * silu(z)
       }
     };
-    if (tb >= s0 && tb + 8 <= s1) block(std::true_type{});
-    else block(std::false_type{});
+    if (tb >= s0 && tb + 8 <= s1) {
+      if (((hmask >> sb) & 0xffull) == 0ull) block(std::true_type{}, std::true_type{});
+      else block(std::true_type{}, std::false_type{});
+    } else {
+      block(std::false_type{}, std::false_type{});
+    }
     if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
   }
   if (s1 == L && a.h_last != nullptr && active) {  // state after the row's last step
