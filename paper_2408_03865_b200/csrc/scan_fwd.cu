@@ -209,13 +209,21 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     auto block = [&](auto full_tag, auto nohead_tag) {
       constexpr bool kFull = decltype(full_tag)::value;
       constexpr bool kNoHead = decltype(nohead_tag)::value;
+      // delta of the 8 steps, two at a time (packed fp32x2)
+      float dls[8];
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float2 v2 = make_float2(vv[i] + bias, vv[i + 1] + bias);
+        const float2 d2 = a.softplus ? softplus2(v2) : v2;
+        dls[i] = d2.x;
+        dls[i + 1] = d2.y;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int t = tb + i;
         yy[i] = 0.f;
         if (!kFull && (t < s0 || t >= s1)) continue;  // CTA-uniform
-        const float v = vv[i] + bias;
-        const float delta = a.softplus ? softplusf(v) : v;
+        const float delta = dls[i];
         const float2 dux2 = f2(delta * uu[i]), dl2 = f2(delta);
         const float2* Bt = reinterpret_cast<const float2*>(sB[sb + i]);
         const float2* Ct = reinterpret_cast<const float2*>(sC[sb + i]);
