@@ -88,8 +88,8 @@ PM_DEV float softplusf(float v) {
 }
 // Two at once with packed fp32x2 arithmetic (same operations and rounding
 // as softplus_x per lane; FFMA2/FMUL2 are bit-identical to the scalar ops).
-PM_DEV float2 softplus2(float2 v) {
-  const float2 x = ex2x2(fmul2(v, f2(kLog2e)));
+PM_DEV float2 softplus2_x(float2 v, float2& x) {
+  x = ex2x2(fmul2(v, f2(kLog2e)));
   float2 q = ffma2(x, f2(0.2f), f2(-0.25f));
   q = ffma2(x, q, f2(0.33333334f));
   q = ffma2(x, q, f2(-0.5f));
@@ -99,6 +99,10 @@ PM_DEV float2 softplus2(float2 v) {
   const float2 l = fmul2(make_float2(lg2(onex.x), lg2(onex.y)), f2(kLn2));
   return make_float2(v.x > 20.f ? v.x : (x.x < 0.03125f ? pp.x : l.x),
                      v.y > 20.f ? v.y : (x.y < 0.03125f ? pp.y : l.y));
+}
+PM_DEV float2 softplus2(float2 v) {
+  float2 x;
+  return softplus2_x(v, x);
 }
 
 // ----------------------------------------------------------------- I/O ----

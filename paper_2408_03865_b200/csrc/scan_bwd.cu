@@ -227,16 +227,28 @@ scan_bwd_kernel(const ScanBwdArgs a) {
         load8<T, false>(dy_row, cb + 8 * hf, L, yy);
         if constexpr (kGate) load8<T, false>(z_row, cb + 8 * hf, L, zz);
       }
+      // delta and softplus'(v) of my 8 steps, two at a time (packed fp32x2)
+      float dls[8], sgs[8];
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float2 v2 = make_float2(vv[i] + bias, vv[i + 1] + bias);
+        if (a.softplus) {
+          float2 x2;
+          const float2 d2 = softplus2_x(v2, x2);
+          dls[i] = d2.x;
+          dls[i + 1] = d2.y;
+          sgs[i] = v2.x > 20.f ? 1.f : __fdividef(x2.x, 1.f + x2.x);
+          sgs[i + 1] = v2.y > 20.f ? 1.f : __fdividef(x2.y, 1.f + x2.y);
+        } else {
+          dls[i] = v2.x;
+          dls[i + 1] = v2.y;
+          sgs[i] = sgs[i + 1] = 1.f;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int ii = 8 * hf + i;
-        const float v = vv[i] + bias;
-        float dl = v, sg = 1.f;
-        if (a.softplus) {
-          float x;
-          dl = softplus_x(v, x);
-          sg = v > 20.f ? 1.f : __fdividef(x, 1.f + x);
-        }
+        const float dl = dls[i], sg = sgs[i];
         float dyv = yy[i];
         if constexpr (kGate) {  // out = y silu(z): dy = dout silu(z), dz = dout silu'(z) y
           const float sz = sigmoidf_fast(zz[i]);
