@@ -238,7 +238,13 @@ PM_API pm_status pm_selective_scan_bwd(const void* u, const void* dt,
  *     always a head (the base ABI).
  *   h_last (optional, (R,Dn,N) fp32): written with the state after slot L-1
  *     (the input of the next part of a cut sequence).
- * At least one of out, states, h_last must be non-NULL.  Pointers are device
+ *   decay (optional, (R,Dn,N) fp32): d h_last / d h0 = prod_t abar_t over the
+ *     row -- exp(A[d,n] * sum_t delta_t) when no slot of the row is a head
+ *     (under the h0 rule above), else 0.  With (decay, h_last) of a local
+ *     pass (h0 = 0) the rows of a cut sequence compose as
+ *     h_last = decay * h0 + h_last_local (the "(prod abar, h) row summaries"
+ *     of a context-parallel scan).
+ * At least one of out, states, h_last, decay must be non-NULL.  Pointers are device
  * memory owned by the caller; h0/h_last must not alias. */
 PM_API pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt,
                                    const float* A, const void* B,
@@ -246,8 +252,8 @@ PM_API pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt,
                                    const float* dt_bias, int32_t dt_softplus,
                                    int32_t zoh, const int32_t* pos,
                                    const void* z, const float* h0, void* out,
-                                   float* states,
-                                   float* h_last, int64_t R, int64_t Dn,
+                                   float* states, float* h_last, float* decay,
+                                   int64_t R, int64_t Dn,
                                    int64_t L, int32_t N, pm_dtype io,
                                    pm_stream_t stream);
 

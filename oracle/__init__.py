@@ -76,6 +76,7 @@ def lib():
         L.pmo_seq_scan_bwd.argtypes = ([_f64p] * 7 + [_i32] + [_f64p] * 8 +
                                        [_i64, _i64, _i32])
         L.pmo_scan_fwd_ext.argtypes = ([_f64p] * 7 + [_i32, _i32, _i32p, _f64p, _f64p, _f64p, _f64p,
+                                        _f64p,
                                         _i64, _i64, _i64, _i32])
         L.pmo_scan_bwd_ext.argtypes = ([_f64p] * 7 + [_i32, _i32, _i32p] + [_f64p] * 13 +
                                        [_i64, _i64, _i64, _i32])
@@ -288,7 +289,8 @@ def seq_scan_bwd(u, dt, A, B, C, D, dt_bias, dy, acc, softplus=True):
 
 # --- NEXT-1 / NEXT-2: gate and state passing ---------------------------------
 
-def scan_fwd_ext(u, dt, A, B, C, D, dt_bias, pos, z=None, h0=None, softplus=True, zoh=False):
+def scan_fwd_ext(u, dt, A, B, C, D, dt_bias, pos, z=None, h0=None, softplus=True, zoh=False,
+                 want_decay=False):
     """Returns (out, h_last): out = y * silu(z) (y if z is None); h0 (R,Dn,N)
     is the state entering t=0 when pos[r,0] != 0; zoh selects Eq 2b
      for B-bar instead of Euler."""
@@ -299,10 +301,13 @@ def scan_fwd_ext(u, dt, A, B, C, D, dt_bias, pos, z=None, h0=None, softplus=True
     N = A.shape[1]
     out = np.empty_like(u)
     h_last = np.empty((R, Dn, N))
+    decay = np.empty((R, Dn, N))
     lib().pmo_scan_fwd_ext(_p(u), _p(dt), _p(A), _p(B), _p(C), _p(D), _p(dt_bias),
                            int(bool(softplus)), int(bool(zoh)), _p(pos, _i32p), _p(z), _p(h0),
                            _p(out),
-                           _p(h_last), R, Dn, L, N)
+                           _p(h_last), _p(decay), R, Dn, L, N)
+    if want_decay:
+        return out, h_last, decay
     return out, h_last
 
 

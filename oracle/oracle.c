@@ -568,12 +568,15 @@ void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
                       const double* B, const double* C, const double* D,
                       const double* dt_bias, int32_t softplus, int32_t zoh,
                       const int32_t* pos, const double* z, const double* h0,
-                      double* out, double* h_last,
+                      double* out, double* h_last, double* decay,
                       int64_t R, int64_t Dn, int64_t L, int32_t N) {
 #pragma omp parallel for collapse(2) schedule(static)
     for (int64_t r = 0; r < R; ++r)
         for (int64_t d = 0; d < Dn; ++d) {
             double* h = (double*)calloc((size_t)N, sizeof(double));
+            /* P = d h_last / d h0 = product of the recurrence multipliers */
+            double* P = (double*)malloc(sizeof(double) * (size_t)N);
+            for (int32_t n = 0; n < N; ++n) P[n] = 1.0;
             const int64_t lane = (r * Dn + d) * L;
             if (h0)
                 for (int32_t n = 0; n < N; ++n) h[n] = h0[(r * Dn + d) * N + n];
@@ -588,6 +591,7 @@ void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
                     double bfac = zoh ? zoh_f(delta * A[d * N + n]) * delta : delta;
                     double bx = bfac * B[(r * N + n) * L + t] * x;
                     h[n] = head ? bx : exp(delta * A[d * N + n]) * h[n] + bx;
+                    P[n] = head ? 0.0 : exp(delta * A[d * N + n]) * P[n];
                     yt += C[(r * N + n) * L + t] * h[n];
                 }
                 yt += (D ? D[d] : 0.0) * x;
@@ -599,7 +603,10 @@ void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
             }
             if (h_last)
                 for (int32_t n = 0; n < N; ++n) h_last[(r * Dn + d) * N + n] = h[n];
+            if (decay)
+                for (int32_t n = 0; n < N; ++n) decay[(r * Dn + d) * N + n] = P[n];
             free(h);
+            free(P);
         }
 }
 

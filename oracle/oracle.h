@@ -132,7 +132,7 @@ void pmo_scan_fwd_ext(const double* u, const double* dt, const double* A,
                       const double* B, const double* C, const double* D,
                       const double* dt_bias, int32_t softplus, int32_t zoh,
                       const int32_t* pos, const double* z, const double* h0,
-                      double* out, double* h_last,
+                      double* out, double* h_last, double* decay,
                       int64_t R, int64_t Dn, int64_t L, int32_t N);
 void pmo_scan_bwd_ext(const double* u, const double* dt, const double* A,
                       const double* B, const double* C, const double* D,

@@ -80,7 +80,7 @@ def lib():
         L.pm_selective_scan_bwd_workspace.argtypes = [_i64, _i64, _i64, _i32, _i32]
         L.pm_selective_scan_bwd.argtypes = ([_vp] * 7 + [_i32] + [_vp] * 10 + [_vp, _sz] +
                                             [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
-        L.pm_selective_scan_fwd_ex.argtypes = ([_vp] * 7 + [_i32, _i32] + [_vp] * 6 +
+        L.pm_selective_scan_fwd_ex.argtypes = ([_vp] * 7 + [_i32, _i32] + [_vp] * 7 +
                                                [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
         L.pm_selective_scan_bwd_ex.argtypes = ([_vp] * 7 + [_i32, _i32] + [_vp] * 15 + [_vp, _sz] +
                                                [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
@@ -313,11 +313,13 @@ def pm_selective_scan_bwd(u, dt, A, B, C, Dskip, dt_bias, pos, dy, states=None,
 
 def pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, z=None, h0=None, out=None,
                              states=None, h_last=None, dt_softplus=True, want_states=True,
-                             want_last_state=False, zoh=False):
+                             want_last_state=False, zoh=False, decay=None, want_decay=False):
     """Extended ScanOp_pack forward: fused gate ``out = y * silu(z)`` (SURVEY
     NEXT-1) and cross-row state passing ``h0 -> h_last`` (NEXT-2, the
     paper's future work P:275); ``zoh`` selects Eq 2b's B-bar (NEXT-4)
-    instead of Euler.  Returns (out, states, h_last)."""
+    instead of Euler.  ``decay`` (R,Dn,N) receives d h_last / d h0 (the row
+    summary of a context-parallel scan).  Returns (out, states, h_last), plus
+    decay when want_decay."""
     import torch
     _dev(u, dt, A, B, C, Dskip, dt_bias, pos, z, h0)
     R, Dn, L = u.shape
@@ -328,12 +330,16 @@ def pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, z=None, h0=Non
         states = torch.empty(nb // 4, dtype=torch.float32, device=u.device)
     if h_last is None and want_last_state:
         h_last = torch.empty((R, Dn, N), dtype=torch.float32, device=u.device)
-    _dev(out, states, h_last)
+    if decay is None and want_decay:
+        decay = torch.empty((R, Dn, N), dtype=torch.float32, device=u.device)
+    _dev(out, states, h_last, decay)
     _check(lib().pm_selective_scan_fwd_ex(
         _ptr(u), _ptr(dt), _ptr(A), _ptr(B), _ptr(C), _ptr(Dskip), _ptr(dt_bias),
         int(bool(dt_softplus)), int(bool(zoh)), _ptr(pos), _ptr(z), _ptr(h0), _ptr(out),
         _ptr(states),
-        _ptr(h_last), R, Dn, L, N, _io(u), _stream(u)), "pm_selective_scan_fwd_ex")
+        _ptr(h_last), _ptr(decay), R, Dn, L, N, _io(u), _stream(u)), "pm_selective_scan_fwd_ex")
+    if want_decay:
+        return out, states, h_last, decay
     return out, states, h_last
 
 

@@ -39,15 +39,17 @@ pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt, const float* A
                                    const float* dt_bias, int32_t dt_softplus, int32_t zoh,
                                    const int32_t* pos, const void* z, const float* h0, void* out,
                                    float* states,
-                                   float* h_last, int64_t R, int64_t Dn, int64_t L, int32_t N,
+                                   float* h_last, float* decay, int64_t R, int64_t Dn, int64_t L,
+                                   int32_t N,
                                    pm_dtype io, pm_stream_t stream) {
   pm_status st = check_common(R, Dn, L, N, io);
   if (st != PM_OK) return st;
-  if (!u || !dt || !A || !B || !C || !pos || (!out && !states && !h_last)) return PM_ERR_INVALID_ARG;
+  if (!u || !dt || !A || !B || !C || !pos || (!out && !states && !h_last && !decay))
+    return PM_ERR_INVALID_ARG;
   for (const void* p : {u, dt, B, C, z, (const void*)out})
     if (!elem_aligned(p, io)) return PM_ERR_ALIGN;
   for (const void* p : {(const void*)A, (const void*)Dskip, (const void*)dt_bias, (const void*)pos,
-                        (const void*)h0, (const void*)h_last})
+                        (const void*)h0, (const void*)h_last, (const void*)decay})
     if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
   if (!aligned16(states)) return PM_ERR_ALIGN;
   const int isz = io == PM_F32 ? 4 : 2;
@@ -55,7 +57,7 @@ pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt, const float* A
                    aligned16(C) && aligned16(out) && aligned16(z);
   ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, out, states, nullptr, nullptr, 0,
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
-                z, h0, h_last, zoh ? 1 : 0};
+                z, h0, h_last, decay, zoh ? 1 : 0};
   if (states != nullptr) {  // persistent longest-first schedule lives in the states buffer
     Sched sc = sched_of(states, R, Dn, L, N);
     a.items = sc.sorted;
@@ -73,7 +75,7 @@ pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, c
                                 pm_stream_t stream) {
   if (!y && !states) return PM_ERR_INVALID_ARG;
   return pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, 0, pos, nullptr,
-                                  nullptr, y, states, nullptr, R, Dn, L, N, io, stream);
+                                  nullptr, y, states, nullptr, nullptr, R, Dn, L, N, io, stream);
 }
 
 pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A, const void* B,
@@ -118,7 +120,7 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
     float* st_ws = reinterpret_cast<float*>(w);
     ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws, nullptr, nullptr, 0,
                    (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
-                   nullptr, h0, nullptr, zoh ? 1 : 0};
+                   nullptr, h0, nullptr, nullptr, zoh ? 1 : 0};
     Sched sc = sched_of(st_ws, R, Dn, L, N);
     fa.items = sc.sorted;
     fa.counter = sc.counters;

@@ -169,6 +169,8 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   // B/C/head tiles are restaged at every kTile boundary.  Sub-blocks fully
   // inside the segment (all but at most two) run without per-step checks.
   int tb = s0 & ~7;
+  float sdl = 0.f;    // sum of delta over the segment (decay summary)
+  bool anyh = false;  // a head inside the segment
   Raw8<T, kVec> pu, pt, pz;
   pu.load(u_row, tb, L);
   pt.load(dt_row, tb, L);
@@ -206,18 +208,18 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     }
     // kFull: all 8 steps inside the segment; kNoHead: and none is a head
     // (most blocks) -- no per-step check at all
+    // delta of the 8 steps, two at a time (packed fp32x2)
+    float dls[8];
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      const float2 v2 = make_float2(vv[i] + bias, vv[i + 1] + bias);
+      const float2 d2 = a.softplus ? softplus2(v2) : v2;
+      dls[i] = d2.x;
+      dls[i + 1] = d2.y;
+    }
     auto block = [&](auto full_tag, auto nohead_tag) {
       constexpr bool kFull = decltype(full_tag)::value;
       constexpr bool kNoHead = decltype(nohead_tag)::value;
-      // delta of the 8 steps, two at a time (packed fp32x2)
-      float dls[8];
-#pragma unroll
-      for (int i = 0; i < 8; i += 2) {
-        const float2 v2 = make_float2(vv[i] + bias, vv[i + 1] + bias);
-        const float2 d2 = a.softplus ? softplus2(v2) : v2;
-        dls[i] = d2.x;
-        dls[i + 1] = d2.y;
-      }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int t = tb + i;
@@ -262,6 +264,26 @@ scan_fwd_kernel(const ScanFwdArgs a) {
       block(std::false_type{}, std::false_type{});
     }
     if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
+    if (a.decay != nullptr) {  // NEXT-2 row summary: sum of delta, any head
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (tb + i >= s0 && tb + i < s1) {
+          sdl += dls[i];
+          anyh = anyh || ((hmask >> (sb + i)) & 1ull);
+        }
+      }
+    }
+  }
+  if (s1 == L && a.decay != nullptr && active) {
+    // d h_last / d h0 = prod_t abar_t = exp(A sum_t delta_t) when no slot of
+    // the row is a head (the whole row is then one segment), else 0
+    float* dp = a.decay + ((int64_t)r * Dn + d) * N;
+    const bool live = s0 == 0 && !anyh;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      dp[2 * p] = live ? ex2(A2[p].x * sdl) : 0.f;
+      dp[2 * p + 1] = live ? ex2(A2[p].y * sdl) : 0.f;
+    }
   }
   if (s1 == L && a.h_last != nullptr && active) {  // state after the row's last step
     float* hp = a.h_last + ((int64_t)r * Dn + d) * N;

@@ -65,6 +65,7 @@ struct ScanFwdArgs {
   const void* z;      // NEXT-1 gate (R,Dn,L) or NULL: y <- y * silu(z)
   const float* h0;    // NEXT-2 state entering t=0 (R,Dn,N) or NULL
   float* h_last;      // state after step L-1 (R,Dn,N) or NULL
+  float* decay;       // d h_last / d h0 (R,Dn,N) or NULL (NEXT-2 row summary)
   int zoh;             // NEXT-4: Eq 2b discretisation of B-bar (else Euler, Q1)
 };
 

@@ -90,9 +90,12 @@ def test_validation_before_launch():
                                    None) == 5
     # extended scan: z requires dz (and vice versa); out/states/h_last all NULL
     ex_f = lambda *a: L.pm_selective_scan_fwd_ex(*a)
-    assert ex_f(*([p] * 7), 1, 0, p, None, None, None, None, None, 2, 8, 64, 16, 0, None) == 1
-    assert ex_f(*([p] * 7), 1, 1, p, _vp(0x1002), None, p, None, None, 2, 8, 64, 16, 0,
+    assert ex_f(*([p] * 7), 1, 0, p, None, None, None, None, None, None, 2, 8, 64, 16, 0,
+                None) == 1
+    assert ex_f(*([p] * 7), 1, 1, p, _vp(0x1002), None, p, None, None, None, 2, 8, 64, 16, 0,
                 None) == 5
+    assert ex_f(*([p] * 7), 1, 0, p, None, None, None, None, None, _vp(0x1002), 2, 8, 64, 16,
+                0, None) == 5  # misaligned decay
     ebase = [p] * 7 + [1, 0, p]
     tail = [ws, 2, 8, 64, 16, 0, None]
     # z given, dz missing

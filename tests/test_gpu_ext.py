@@ -182,3 +182,48 @@ def test_zoh_recompute_equals_saved():
     assert torch.equal(a[0], b[0])
     for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dz", "dh0"):
         assert torch.equal(a[2][k], b[2][k]), k
+
+
+# --------------------------------------------------------------------------
+# NEXT-2 row summaries: decay = d h_last / d h0, context-parallel composition
+# --------------------------------------------------------------------------
+
+def test_decay_parity():
+    pos, u, T, P, z, h0, dh = problem(4, 96, 512, 16, "one", "f32", seed=95, continued=(0, 2))
+    out, st, hl, dec = pm.pm_selective_scan_fwd_ex(u, T["dt"], P["A"], T["B"], T["C"], P["D"],
+                                                   P["dt_bias"], pos, h0=h0, want_last_state=True,
+                                                   want_decay=True)
+    torch.cuda.synchronize()
+    args = (to_np(u), to_np(T["dt"]), to_np(P["A"]), to_np(T["B"]), to_np(T["C"]),
+            to_np(P["D"]), to_np(P["dt_bias"]), to_np(pos).astype(np.int32))
+    _, rhl, rdec = oracle.scan_fwd_ext(*args, h0=to_np(h0), want_decay=True)
+    assert rel_err(to_np(dec), rdec) <= 1e-4
+    assert rel_err(to_np(hl), rhl) <= 1e-4
+    d = to_np(dec)
+    assert np.all(d[1] == 0) and np.all(d[3] == 0)  # rows that start a sequence
+    assert np.any(d[0] > 0) and np.any(d[2] > 0)  # (exp underflows to 0 for large sums)
+
+
+def test_context_parallel_scan_over_rows():
+    """One long sequence cut into 4 rows of one launch: a local pass (h0 = 0)
+    gives each row's (decay, h_last); composing them row by row gives every
+    row's true h0, and a second pass reproduces the uncut sequence (oracle)."""
+    G, L, Dn, N = 4, 256, 64, 16
+    pos, u, T, P, z, h0, dh = problem(G, Dn, L, N, "one", "f32", seed=96)
+    pos = (torch.arange(G * L, device="cuda", dtype=torch.int32).view(G, L)).contiguous()
+    zero = torch.zeros((G, Dn, N), device="cuda")
+    _, _, hl, dec = pm.pm_selective_scan_fwd_ex(u, T["dt"], P["A"], T["B"], T["C"], P["D"],
+                                                P["dt_bias"], pos, h0=zero, want_last_state=True,
+                                                want_decay=True)
+    hin = torch.zeros_like(zero)
+    for k in range(1, G):  # the exchange: G x (Dn x N) summaries
+        hin[k] = dec[k - 1] * hin[k - 1] + hl[k - 1]
+    out, _, hl2 = pm.pm_selective_scan_fwd_ex(u, T["dt"], P["A"], T["B"], T["C"], P["D"],
+                                              P["dt_bias"], pos, h0=hin, want_last_state=True)
+    torch.cuda.synchronize()
+    cat = lambda t: np.concatenate(list(to_np(t)), axis=-1)[None]  # rows -> one long row
+    args = (cat(u), cat(T["dt"]), to_np(P["A"]), cat(T["B"]), cat(T["C"]), to_np(P["D"]),
+            to_np(P["dt_bias"]), np.arange(G * L, dtype=np.int32)[None])
+    ro, rhl = oracle.scan_fwd_ext(*args)
+    assert rel_err(cat(out), ro) <= 1e-4
+    assert rel_err(to_np(hl2)[-1], rhl[0]) <= 1e-4

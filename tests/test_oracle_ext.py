@@ -130,3 +130,36 @@ def test_state_passing_reproduces_the_uncut_row():
         assert np.array_equal(np.concatenate([g1[k], g2[k]], -1), g[k]), k
     for k in ("dA", "dD", "ddt_bias"):
         np.testing.assert_allclose(g1[k] + g2[k], g[k], rtol=1e-12, atol=1e-12)
+
+
+def test_decay_row_summary():
+    """decay = d h_last / d h0 (NEXT-2's (prod abar, h) row summary): equals
+    exp(A sum delta) on rows without a head, 0 on rows with one, and
+    h_last(h0) = decay * h0 + h_last(0) exactly up to rounding (linearity)."""
+    rng = np.random.default_rng(40)
+    R, Dn, L, N = 3, 2, 12, 3
+    _, pos, _, P = rand_problem(rng, R, Dn, L, N, 4, [[L], [L], [5, 7]])
+    pos[0] += 4  # row 0 continues a sequence: no head anywhere
+    pos[1, :4] = [2, 3, 4, 5]  # row 1 continues, then a head at slot 4
+    pos[1, 4:] = np.arange(L - 4)
+    u = rng.standard_normal((R, Dn, L))
+    h0 = rng.standard_normal((R, Dn, N))
+    args = (u, P["dt"], P["A"], P["B"], P["C"], P["D"], P["dt_bias"], pos)
+    for zoh in (False, True):
+        _, hl, dec = oracle.scan_fwd_ext(*args, h0=h0, zoh=zoh, want_decay=True)
+        _, hl0, dec0 = oracle.scan_fwd_ext(*args, h0=np.zeros_like(h0), zoh=zoh, want_decay=True)
+        assert np.array_equal(dec, dec0)
+        delta = np.logaddexp(0.0, P["dt"] + P["dt_bias"][None, :, None])
+        closed = np.exp(P["A"][None] * delta.sum(-1)[:, :, None])
+        np.testing.assert_allclose(dec[0], closed[0], rtol=1e-12)
+        assert np.all(dec[1] == 0) and np.all(dec[2] == 0)
+        np.testing.assert_allclose(hl, dec * h0 + hl0, rtol=1e-12, atol=1e-13)
+        # finite differences of h_last in h0 (diagonal Jacobian)
+        eps = 1e-6
+        for idx in [(0, 0, 0), (0, 1, 2), (1, 1, 1)]:
+            hp, hm = h0.copy(), h0.copy()
+            hp[idx] += eps
+            hm[idx] -= eps
+            fd = (oracle.scan_fwd_ext(*args, h0=hp, zoh=zoh)[1][idx] -
+                  oracle.scan_fwd_ext(*args, h0=hm, zoh=zoh)[1][idx]) / (2 * eps)
+            assert abs(fd - dec[idx]) < 1e-8
