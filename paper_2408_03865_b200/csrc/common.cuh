@@ -2,6 +2,7 @@
 // (Product path.  Shares nothing with oracle/.)
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors; no driver library link needed)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -270,6 +271,53 @@ struct Raw8<__nv_bfloat16, true> {
     }
   }
 };
+
+// ----------------------------------------------------- TMA + mbarrier ----
+// Bulk tensor copies (cp.async.bulk.tensor, SASS UTMALDG) complete on a
+// shared-memory mbarrier that counts the transferred bytes.
+PM_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+PM_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+PM_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+PM_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+template <int D>
+PM_DEV void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2 = 0,
+                     int c3 = 0) {
+  const uint64_t m = reinterpret_cast<uint64_t>(map);
+  if constexpr (D == 2) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)), "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+  } else if constexpr (D == 3) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(smem_u32(dst)), "l"(m), "r"(smem_u32(bar)), "r"(c0),
+        "r"(c1), "r"(c2)
+        : "memory");
+  } else {
+    static_assert(D == 4, "2, 3 or 4 dimensions");
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];\n" ::"r"(smem_u32(dst)), "l"(m), "r"(smem_u32(bar)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+  }
+}
 
 // ------------------------------------------------------------ cp.async ----
 // 16-byte global->shared async copy (LDGSTS); src_bytes < 16 zero-fills.

@@ -1,11 +1,65 @@
 // scan.cu -- C ABI of ScanOp_pack (include/pm.h): argument validation,
 // workspace / states layout, dispatch to the kernels in scan_fwd.cu and
 // scan_bwd.cu.
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
+
 #include "scan_impl.cuh"
 
 namespace {
 
 using namespace pm;
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link
+// against libcuda); resolved once.
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// A tiled, unswizzled map over a dense tensor; dims innermost first, strides
+// in bytes for dims 1..rank-1.  Out-of-range box elements read as zero.
+bool encode_map(CUtensorMap* m, CUtensorMapDataType type, int rank, const void* base,
+                const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
+  const auto enc = tensor_map_encoder();
+  if (enc == nullptr || base == nullptr) return false;
+  const cuuint32_t ones[4] = {1, 1, 1, 1};
+  return enc(m, type, (cuuint32_t)rank, const_cast<void*>(base), dims, strides, box, ones,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA descriptors of the backward's per-chunk inputs (see ScanBwdArgs).
+bool encode_bwd_maps(ScanBwdArgs& a, int N, pm_dtype io) {
+  const CUtensorMapDataType ty = io == PM_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const cuuint64_t isz = io == PM_F32 ? 4 : 2, L = a.L, Dn = a.Dn, R = a.R;
+  const cuuint64_t dtok[3] = {L, Dn, R}, stok[2] = {L * isz, L * Dn * isz};
+  const cuuint32_t btok[3] = {kChunk, kBwdCh, 1};
+  const cuuint64_t dbc[3] = {L, (cuuint64_t)N, R}, sbc[2] = {L * isz, L * N * isz};
+  const cuuint32_t bbc[3] = {kChunk, (cuuint32_t)N, 1};
+  const cuuint64_t dpos[2] = {L, R}, spos[1] = {L * 4};
+  const cuuint32_t bpos[2] = {kChunk, 1};
+  const cuuint64_t nch = a.nchunk;
+  const cuuint64_t dst[4] = {Dn, (cuuint64_t)N, nch, R},
+                   sst[3] = {Dn * 4, Dn * N * 4, Dn * N * nch * 4};
+  const cuuint32_t bst[4] = {kBwdCh, (cuuint32_t)N, 1, 1};
+  bool ok = encode_map(&a.tm_u, ty, 3, a.u, dtok, stok, btok) &&
+            encode_map(&a.tm_dt, ty, 3, a.dt, dtok, stok, btok) &&
+            encode_map(&a.tm_dy, ty, 3, a.dy, dtok, stok, btok) &&
+            encode_map(&a.tm_B, ty, 3, a.B, dbc, sbc, bbc) &&
+            encode_map(&a.tm_C, ty, 3, a.C, dbc, sbc, bbc) &&
+            encode_map(&a.tm_pos, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, a.pos, dpos, spos, bpos) &&
+            encode_map(&a.tm_st, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.states, dst, sst, bst);
+  if (ok && a.z != nullptr) ok = encode_map(&a.tm_z, ty, 3, a.z, dtok, stok, btok);
+  return ok;
+}
 
 // bwd workspace = dB/dC partials | param partials | counter | (recomputed states)
 size_t ws_bc_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
@@ -137,6 +191,11 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
                 sc.sorted, counter, (int)(R * n_seg(L)),
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
                 z, h0, dh_last, dz, dh0, zoh ? 1 : 0};
+  // TMA for the per-chunk inputs when the vector path applies (row strides
+  // are then multiples of 16 bytes); cp.async otherwise.  PM_NO_TMA=1 forces
+  // cp.async (A/B measurements).
+  a.use_tma = vec && Dn % 4 == 0 && getenv("PM_NO_TMA") == nullptr &&
+              encode_bwd_maps(a, (int)N, io) ? 1 : 0;
   return run_scan_bwd(a, (int)N, vec, io, dA, dB, dC, dD, ddt_bias, s);
 }
 

@@ -30,15 +30,15 @@ namespace pm {
 //            chunk's du/ddt rows leave with full-sector vector stores.
 
 template <typename T, int N, bool kGate>
-struct BwdRaw {  // raw inputs of one chunk, filled by cp.async (vector path)
-  T u[kBwdCh][kChunk];
-  T dt[kBwdCh][kChunk];
-  T dy[kBwdCh][kChunk];
-  T z[kGate ? kBwdCh : 1][kChunk];
-  T B[N][kChunk];
-  T C[N][kChunk];
-  int32_t pos[kChunk];
-  float st[N][kBwdCh];
+struct BwdRaw {  // raw inputs of one chunk, filled by TMA or cp.async (vector path)
+  alignas(128) T u[kBwdCh][kChunk];
+  alignas(128) T dt[kBwdCh][kChunk];
+  alignas(128) T dy[kBwdCh][kChunk];
+  alignas(128) T B[N][kChunk];
+  alignas(128) T C[N][kChunk];
+  alignas(128) int32_t pos[kChunk];
+  alignas(128) float st[N][kBwdCh];
+  alignas(128) T z[kGate ? kBwdCh : 1][kChunk];
 };
 
 template <typename T, int N, bool kGate>
@@ -55,6 +55,7 @@ struct BwdSmem {
   float4 xw[kChunk / 2][kBwdWarps][kRows][2];
   float B[kChunk][N];
   float C[kChunk][N];
+  uint64_t bar;       // TMA completion barrier of the raw buffer
   unsigned hmask[1];  // head flags of the chunk (bit e = step cb + e)
   int s_red[kBwdWarps];
   uint32_t tmem_base;
@@ -64,10 +65,29 @@ struct BwdSmem {
 // L*isz % 16 == 0, Dn % 4 == 0, 16-byte aligned pointers).
 template <typename T, int N, bool kGate>
 PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, int dblk, int c,
-                          int s0) {
+                          int s0, uint64_t* bar) {
   constexpr int kEl = 16 / (int)sizeof(T);       // elements per 16-byte chunk
   constexpr int kRowQ = kChunk / kEl;            // chunks per (row, chunk)
   const int L = a.L, Dn = a.Dn, cb = c * kChunk;
+  const bool with_st = cb > s0 || (cb == 0 && a.h0 != nullptr);
+  if (a.use_tma) {  // one thread issues the chunk's bulk tensor copies
+    if (threadIdx.x == 0) {
+      constexpr uint32_t kRows = kBwdCh * kChunk * sizeof(T);
+      const uint32_t bytes = (kGate ? 4 : 3) * kRows + 2 * N * kChunk * sizeof(T) +
+                             kChunk * sizeof(int32_t) + (with_st ? N * kBwdCh * sizeof(float) : 0);
+      mbar_expect_tx(bar, bytes);
+      const int d0 = dblk * kBwdCh;
+      tma_load<3>(rw.u, &a.tm_u, bar, cb, d0, r);
+      tma_load<3>(rw.dt, &a.tm_dt, bar, cb, d0, r);
+      tma_load<3>(rw.dy, &a.tm_dy, bar, cb, d0, r);
+      if constexpr (kGate) tma_load<3>(rw.z, &a.tm_z, bar, cb, d0, r);
+      tma_load<3>(rw.B, &a.tm_B, bar, cb, 0, r);
+      tma_load<3>(rw.C, &a.tm_C, bar, cb, 0, r);
+      tma_load<2>(rw.pos, &a.tm_pos, bar, cb, r);
+      if (with_st) tma_load<4>(rw.st, &a.tm_st, bar, d0, 0, c, r);
+    }
+    return;
+  }
   constexpr int kTx = kBwdCh * kRowQ;
 #pragma unroll
   for (int arr = 0; arr < (kGate ? 4 : 3); ++arr) {  // u, dt, dy (, z)
@@ -96,7 +116,7 @@ PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, 
     const bool ok = t0 < L;
     cp_async16(&rw.pos[4 * e], a.pos + (int64_t)r * L + (ok ? t0 : 0), ok ? 16 : 0);
   }
-  if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
+  if (with_st) {
     for (int e = threadIdx.x; e < N * (kBwdCh / 4); e += kBwdThreads) {
       const int n = e / (kBwdCh / 4), q = e % (kBwdCh / 4);
       const int d0 = dblk * kBwdCh + 4 * q;
@@ -110,7 +130,7 @@ PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, 
 
 template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh>
 __global__ void __launch_bounds__(kBwdThreads, MinB)
-scan_bwd_kernel(const ScanBwdArgs a) {
+scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   using SM = BwdSmem<T, N, kGate>;
   constexpr int NH = SM::NH, kQ = SM::kQ, kRows = SM::kRows;
@@ -126,6 +146,8 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   // SM's 512 columns) instead of registers or shared memory.
   constexpr uint32_t kTmemCols = (kChunk * NH <= 32) ? 32u : (kChunk * NH <= 64 ? 64u : 128u);
   if (wid == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
+  if (tid == 32) mbar_init(&sm.bar, 1);
+  uint32_t bar_phase = 0;
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -200,7 +222,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
   float dD = 0.f, ddtb = 0.f;
 
   const int cfirst = s0 / kChunk, clast = (s1 - 1) / kChunk;
-  if constexpr (kVec) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, clast, s0);
+  if constexpr (kVec) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, clast, s0, &sm.bar);
   if (s1 == L && a.dh_last != nullptr) {  // NEXT-2: cotangent of the carried-out state
     const float* gp = a.dh_last + ((int64_t)r * Dn + d) * N + n0;
 #pragma unroll
@@ -210,7 +232,14 @@ scan_bwd_kernel(const ScanBwdArgs a) {
 
   for (int c = clast; c >= cfirst; --c) {
     const int cb = c * kChunk, c0 = max(cb, s0), c1 = min(cb + kChunk, s1);
-    if constexpr (kVec) cp_async_wait_all();
+    if constexpr (kVec) {
+      if (a.use_tma) {
+        mbar_wait(&sm.bar, bar_phase);
+        bar_phase ^= 1u;
+      } else {
+        cp_async_wait_all();
+      }
+    }
     __syncthreads();  // raw chunk visible; previous chunk's smem readers done
     // ---- phase 1: scalars, B/C, head, chunk start state ----
     float2 h[NP];
@@ -295,7 +324,7 @@ scan_bwd_kernel(const ScanBwdArgs a) {
     __syncthreads();  // scalars visible; raw buffer free
     const uint32_t hmask = sm.hmask[0];  // head flags of the chunk (CTA-uniform register)
     if constexpr (kVec) {
-      if (c > cfirst) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, c - 1, s0);
+      if (c > cfirst) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, c - 1, s0, &sm.bar);
     }
 
     auto passes = [&](auto full_tag) {

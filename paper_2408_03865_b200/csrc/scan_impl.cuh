@@ -94,6 +94,11 @@ struct ScanBwdArgs {
   void* dz;             // (R,Dn,L) when z != NULL
   float* dh0;           // (R,Dn,N) when h0 != NULL
   int zoh;              // NEXT-4: Eq 2b discretisation of B-bar (else Euler, Q1)
+  // TMA descriptors of the per-chunk inputs (vector path; use_tma = 0 falls
+  // back to cp.async): (L, Dn, R) u/dt/dy/z, (L, N, R) B/C, (L, R) pos,
+  // (Dn, N, nchunk, R) states
+  int use_tma;
+  CUtensorMap tm_u, tm_dt, tm_dy, tm_z, tm_B, tm_C, tm_pos, tm_st;
 };
 
 // ---------------------------------------------------------------------------

@@ -256,3 +256,15 @@ def test_many_rows_bucket_sorted_schedule():
     for k in ("u", "y", "du", "ddt", "dB", "dC", "dx"):
         assert torch.equal(out[k][sub], o2[k]), k
     check_chain(pos[sub].contiguous(), Ts, P, o2, "f32")
+
+
+def test_tma_and_cp_async_staging_agree(monkeypatch):
+    """The backward stages its per-chunk inputs with TMA (bulk tensor copies)
+    when the vector path applies; PM_NO_TMA=1 selects cp.async.  Same
+    arithmetic, so the results are bit-identical."""
+    rows, pos, valid, T, P = problem(2, 192, 1024, 16, "edges", "bf16", seed=31)
+    a = run_chain(pos, T, P)
+    monkeypatch.setenv("PM_NO_TMA", "1")
+    b = run_chain(pos, T, P)
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dx", "dw", "db"):
+        assert torch.equal(a[k], b[k]), k
