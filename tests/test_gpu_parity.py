@@ -262,7 +262,7 @@ def test_tma_and_cp_async_staging_agree(monkeypatch):
     """The backward stages its per-chunk inputs with TMA (bulk tensor copies)
     when the vector path applies; PM_NO_TMA=1 selects cp.async.  Same
     arithmetic, so the results are bit-identical."""
-    rows, pos, valid, T, P = problem(2, 192, 1024, 16, "edges", "bf16", seed=31)
+    rows, pos, valid, T, P = problem(2, 192, 1024, 16, 4, "edges", "bf16", seed=31)
     a = run_chain(pos, T, P)
     monkeypatch.setenv("PM_NO_TMA", "1")
     b = run_chain(pos, T, P)
