@@ -23,7 +23,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpm.so")
+# PM_LIB: an alternative in-tree build (A/B experiments, tools/gpu_ab_lib.sh)
+LIB_PATH = os.environ.get("PM_LIB") or os.path.join(_HERE, "libpm.so")
 
 PM_F32, PM_BF16 = 0, 1
 STATUS = {0: "PM_OK", 1: "PM_ERR_INVALID_ARG", 2: "PM_ERR_CAPACITY", 3: "PM_ERR_SHAPE",

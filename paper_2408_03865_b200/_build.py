@@ -33,16 +33,19 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in _inputs())
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
+          out: str = LIB, defines: tuple = ()) -> str:
+    """Build libpm.so; `out`/`defines` build a variant (e.g. out=libpm_b.so,
+    defines=("PM_FWD_POLY=0",)) for A/B experiments loaded through PM_LIB."""
+    if out == LIB and not defines and not force and not stale():
         return LIB
     objs = []
-    bdir = os.path.join(HERE, "build")
+    bdir = os.path.join(HERE, "build" if out == LIB else "build_" + os.path.basename(out)[:-3])
     os.makedirs(bdir, exist_ok=True)
     procs = []
     for s in SOURCES:
         o = os.path.join(bdir, s.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, s), "-o", o]
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, s), "-o", o]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         if verbose:
@@ -51,20 +54,23 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
         objs.append(o)
     failed = False
     for p, s in procs:
-        out, _ = p.communicate()
-        if p.returncode != 0 or (ptxas_v and out):
-            sys.stderr.write(out.decode())
+        log, _ = p.communicate()
+        if p.returncode != 0 or (ptxas_v and log):
+            sys.stderr.write(log.decode())
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "shared", "-o", tmp, *objs,
            "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True, ptxas_v="-v" in sys.argv)
-    print(LIB)
+    # python _build.py [--force] [-v] [--out libpm_x.so] [-DNAME=V ...]
+    a = sys.argv[1:]
+    out = os.path.join(HERE, a[a.index("--out") + 1]) if "--out" in a else LIB
+    defs = tuple(x[2:] for x in a if x.startswith("-D"))
+    print(build(force="--force" in a, verbose=True, ptxas_v="-v" in a, out=out, defines=defs))

@@ -450,6 +450,23 @@ PM_DEV void segment_bounds(const int32_t* __restrict__ pos_row, int L, int k, in
 
 }  // namespace pm
 
+// ------------------------------------- cross-kernel / cross-CTA sync ----
+// Programmatic dependent launch: the next kernel in the stream (launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization) may start once every
+// CTA of this one has executed this (its CTAs then take SM slots as this
+// kernel's CTAs exit).
+PM_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+PM_DEV void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+PM_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// generic-proxy writes (another CTA's st.global) before async-proxy reads (TMA)
+PM_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 // host-side error helper
 #define PM_LAUNCH_CHECK()                                     \
   do {                                                        \

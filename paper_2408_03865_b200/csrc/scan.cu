@@ -109,13 +109,14 @@ pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt, const float* A
   const int isz = io == PM_F32 ? 4 : 2;
   const bool vec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
                    aligned16(C) && aligned16(out) && aligned16(z);
-  ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, out, states, nullptr, nullptr, 0,
+  ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, out, states, nullptr, nullptr, nullptr, 0,
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
                 z, h0, h_last, decay, zoh ? 1 : 0};
   if (states != nullptr) {  // persistent longest-first schedule lives in the states buffer
     Sched sc = sched_of(states, R, Dn, L, N);
     a.items = sc.sorted;
     a.counter = sc.counters;
+    a.done = sc.done;
     a.n_items = (int)(R * n_seg(L));
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -172,12 +173,13 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
   const float* stp = states;
   if (recompute) {
     float* st_ws = reinterpret_cast<float*>(w);
-    ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws, nullptr, nullptr, 0,
+    ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws, nullptr, nullptr, nullptr, 0,
                    (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
                    nullptr, h0, nullptr, nullptr, zoh ? 1 : 0};
     Sched sc = sched_of(st_ws, R, Dn, L, N);
     fa.items = sc.sorted;
     fa.counter = sc.counters;
+    fa.done = sc.done;
     fa.n_items = (int)(R * n_seg(L));
     const bool fvec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
                       aligned16(C);
@@ -185,10 +187,12 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
     if (fs != PM_OK) return fs;
     stp = st_ws;
   }
-  // the length-sorted segment list written by the forward pass
+  // the length-sorted segment list, work counters and per-segment done
+  // counts written by the forward pass (in the states buffer)
   const Sched sc = sched_of(const_cast<float*>(stp), R, Dn, L, N);
+  (void)counter;
   ScanBwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, stp, dout, du, ddt, ws_bc, ws_par,
-                sc.sorted, counter, (int)(R * n_seg(L)),
+                sc.sorted, sc.counters + 1, sc.done, (int)(R * n_seg(L)),
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
                 z, h0, dh_last, dz, dh0, zoh ? 1 : 0};
   // TMA for the per-chunk inputs when the vector path applies (row strides

@@ -3,7 +3,13 @@
 // P:224) and its deterministic finalize kernels.
 #include "scan_impl.cuh"
 
+#ifndef PM_BWD_UNROLL  // 2-step rounds unrolled per iteration of the full-chunk reverse pass
+#define PM_BWD_UNROLL 4
+#endif
+
 namespace pm {
+
+constexpr int kBwdUnroll = PM_BWD_UNROLL;
 
 // ---------------------------------------------------------------------------
 // backward
@@ -157,7 +163,21 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
   int r, k, dblk, s0, s1;
   if (a.items != nullptr) {  // persistent: longest segments first
     __syncthreads();
-    if (tid == 0) sm.s_red[0] = atomicAdd(a.counter, 1);
+    if (tid == 0) {
+      const int w = atomicAdd(a.counter, 1);
+      sm.s_red[0] = w;
+      if (w < a.n_items * ndblk && a.done != nullptr) {
+        // this kernel may run while the forward's last items are still in
+        // flight (programmatic launch): wait until every forward channel
+        // block of this segment has released its states (bounded: a states
+        // buffer not written by the forward must not hang the GPU)
+        const int4 it = a.items[w / ndblk];
+        const int* dp = a.done + it.x * a.nseg + it.y;
+        const int need = (a.Dn + kScanThreads - 1) / kScanThreads;  // fwd channel blocks
+        for (int spin = 0; spin < (1 << 22) && ld_acquire(dp) < need; ++spin) __nanosleep(256);
+        fence_proxy_async_global();  // the states are read by TMA (async proxy)
+      }
+    }
     __syncthreads();
     const int w = sm.s_red[0];
     __syncthreads();
@@ -522,7 +542,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
       }
     };
     if constexpr (kFull) {
-#pragma unroll 2
+#pragma unroll kBwdUnroll
       for (int sc = kBNSub - 1; sc >= 0; --sc) sub_chunk(sc);
     } else {
 #pragma unroll 1
@@ -595,6 +615,14 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
     }
   }
   }  // work loop
+  if (a.items != nullptr && tid == 0) {
+    // the last CTA out resets the schedule counters for the next launch
+    // (every CTA has claimed its final, failing ticket by now)
+    if (atomicAdd(a.counter + 1, 1) == (int)gridDim.x - 1) {
+      a.counter[0] = 0;
+      a.counter[1] = 0;
+    }
+  }
   tmem_fence_before();
   __syncthreads();
   if (wid == 0) {
@@ -679,7 +707,9 @@ pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
                            (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
     return PM_ERR_CUDA;
   if (a.items != nullptr) {
-    if (cudaMemsetAsync(a.counter, 0, sizeof(int), s) != cudaSuccess) return PM_ERR_CUDA;
+    // no memset here: the counters are zeroed by the forward's schedule
+    // launch and reset by this kernel's last CTA, so the launch can follow
+    // the forward kernel directly (programmatic dependent launch)
     // resident CTAs per SM: register cap (launch bounds) and 228 KB of shared
     // memory per SM (1 KB reserved per CTA); the occupancy API under-reports
     // this kernel, so the grid is sized from the limits directly.
@@ -691,7 +721,17 @@ pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * nb, items));
     if (getenv("PM_DEBUG"))
       fprintf(stderr, "[pm] bwd persistent grid: %d x %d CTAs/SM (smem %zu) -> %d\n", nsm, nb, smem, g);
-    kern<<<g, kBwdThreads, smem, s>>>(a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(kBwdThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (a.done != nullptr && getenv("PM_NO_PDL") == nullptr) ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return PM_ERR_CUDA;
   } else {
     kern<<<dim3(n_dblk_bwd(a.Dn), a.R, a.nseg), kBwdThreads, smem, s>>>(a);
   }

@@ -105,11 +105,22 @@ scan_fwd_kernel(const ScanFwdArgs a) {
 
   const int L = a.L, Dn = a.Dn;
   const int ndblk = (Dn + kScanThreads - 1) / kScanThreads;
+  // the backward (launched programmatically behind this kernel) takes the SM
+  // slots this kernel's CTAs leave; it waits per segment on a.done
+  pdl_launch_dependents();
   for (int iter = 0;; ++iter) {
   int r, dblk, s0, s1;
   if (a.items != nullptr) {  // persistent: longest segments first
-    __syncthreads();
-    if (threadIdx.x == 0) s_work = atomicAdd(a.counter, 1);
+    __syncthreads();  // the previous item's states / y are written by every thread
+    if (threadIdx.x == 0) {
+      // release the finished item's segment (thread 0 re-reads its item
+      // rather than keeping it in a register across the item)
+      if (iter > 0) {
+        const int4 pv = a.items[s_work / ndblk];
+        red_release_add(a.done + pv.x * a.nseg + pv.y, 1);
+      }
+      s_work = atomicAdd(a.counter, 1);
+    }
     __syncthreads();
     const int w = s_work;
     if (w >= a.n_items * ndblk) break;
@@ -330,7 +341,8 @@ template <typename T, int N, bool kVec>
 pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
   if (a.items != nullptr) {  // schedule: plan + sort (reads pos only), reset counter
     Sched sc = sched_of(a.states, a.R, a.Dn, a.L, N);
-    if (cudaMemsetAsync(sc.counters, 0, 256, s) != cudaSuccess) return PM_ERR_CUDA;
+    if (cudaMemsetAsync(sc.counters, 0, 256 + done_bytes(a.R, a.L), s) != cudaSuccess)
+      return PM_ERR_CUDA;
     seg_plan_kernel<<<a.R, 256, 0, s>>>(a.pos, a.L, a.nseg, sc.unsorted);
     PM_LAUNCH_CHECK();
     seg_sort_kernel<<<1, 1024, 0, s>>>(sc.unsorted, a.n_items, a.L, sc.sorted);

@@ -32,12 +32,21 @@
 
 namespace pm {
 
-constexpr int kScanThreads = 128;
+#ifndef PM_FWD_THREADS
+#define PM_FWD_THREADS 128
+#endif
+#ifndef PM_FWD_MINB
+#define PM_FWD_MINB 4
+#endif
+constexpr int kScanThreads = PM_FWD_THREADS;
 constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kTile = 64;   // fwd staging tile (time steps)
 constexpr int kChunk = 16;  // checkpoint interval (time steps)
-constexpr int kFwdMinB = 4;  // resident fwd CTAs per SM (register cap 128)
-constexpr int kBwdMinB = 4;  // resident bwd CTAs per SM (register cap 128; smem fits 4)
+constexpr int kFwdMinB = PM_FWD_MINB;  // resident fwd CTAs per SM (register cap 128)
+#ifndef PM_BWD_MINB
+#define PM_BWD_MINB 4
+#endif
+constexpr int kBwdMinB = PM_BWD_MINB;  // resident bwd CTAs per SM (register cap 128; smem fits 4)
 
 constexpr int kBwdCh = 64;                   // channels per CTA
 constexpr int kBwdThreads = 2 * kBwdCh;      // lane pair per channel
@@ -60,6 +69,7 @@ struct ScanFwdArgs {
   float* states;
   const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
   int* counter;       // work counter for the persistent loop
+  int* done;          // per-segment finished channel blocks (persistent mode)
   int n_items;
   int R, Dn, L, nseg, nchunk, softplus;
   const void* z;      // NEXT-1 gate (R,Dn,L) or NULL: y <- y * silu(z)
@@ -85,7 +95,8 @@ struct ScanBwdArgs {
   float* ws_bc;     // (nDblk, R, L, 2N)
   float* ws_param;  // (R*nseg, N+2, Dn)
   const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
-  int* counter;
+  int* counter;       // counters[1] of the schedule: work counter; counter[1]: CTAs exited
+  const int* done;    // the fwd's per-segment done counts (wait for n_dblk(Dn) each)
   int n_items;
   int R, Dn, L, nseg, nchunk, softplus;
   const void* z;        // NEXT-1 gate (R,Dn,L) or NULL; dy is then d(out)
@@ -145,18 +156,27 @@ inline int n_dblk_bwd(int64_t Dn) { return (int)((Dn + kBwdCh - 1) / kBwdCh); }
 // the paper's length distribution a segment is ~one sequence), <= 64.
 inline int n_seg(int64_t L) { return (int)std::max<int64_t>(1, std::min<int64_t>(64, L / 256)); }
 
-// states buffer = fp32 chunk states | 256 B counters | sorted segment list |
-// unsorted segment list (the fwd writes the schedule; the bwd reuses it)
+// states buffer = fp32 chunk states | 256 B counters | per-segment done
+// counts | sorted segment list | unsorted segment list (the fwd writes the
+// schedule; the bwd reuses it).  counters[0]: fwd work counter; [1]: bwd
+// work counter; [2]: bwd CTAs exited (the last one resets [1] and [2], so the
+// bwd needs no memset of its own and can launch programmatically right
+// behind the fwd).  done[r*nseg+k]: fwd channel blocks finished on segment
+// (r,k) -- a bwd item starts once its segment's count is complete.
 inline size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
 inline size_t states_f32_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
   return (size_t)R * n_chunks(L) * N * Dn * sizeof(float);
 }
-inline size_t sched_bytes(int64_t R, int64_t L) { return 256 + 2 * up256((size_t)R * n_seg(L) * 16); }
+inline size_t done_bytes(int64_t R, int64_t L) { return up256((size_t)R * n_seg(L) * sizeof(int)); }
+inline size_t sched_bytes(int64_t R, int64_t L) {
+  return 256 + done_bytes(R, L) + 2 * up256((size_t)R * n_seg(L) * 16);
+}
 inline size_t state_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
   return up256(states_f32_bytes(R, Dn, L, N)) + sched_bytes(R, L);
 }
 struct Sched {
   int* counters;
+  int* done;
   int4* sorted;
   int4* unsorted;
 };
@@ -164,8 +184,10 @@ inline Sched sched_of(void* states, int64_t R, int64_t Dn, int64_t L, int32_t N)
   char* b = static_cast<char*>(states) + up256(states_f32_bytes(R, Dn, L, N));
   Sched sc;
   sc.counters = reinterpret_cast<int*>(b);
-  sc.sorted = reinterpret_cast<int4*>(b + 256);
-  sc.unsorted = reinterpret_cast<int4*>(b + 256 + up256((size_t)R * n_seg(L) * 16));
+  sc.done = reinterpret_cast<int*>(b + 256);
+  b += 256 + done_bytes(R, L);
+  sc.sorted = reinterpret_cast<int4*>(b);
+  sc.unsorted = reinterpret_cast<int4*>(b + up256((size_t)R * n_seg(L) * 16));
   return sc;
 }
 

@@ -110,9 +110,11 @@ def test_validation_before_launch():
     assert L.pm_selective_scan_bwd_ex(*ebase, None, None, p, p, _vp(0x1002), *([p] * 7), None,
                                       None, p, *tail) == 5
     # state bytes: (R, ceil(L/16), N, Dn) fp32 states (256-B aligned) + the
-    # segment schedule (256 B counters + 2 lists of R*nseg int4, 256-B aligned)
+    # segment schedule (256 B counters + R*nseg int32 done counts + 2 lists of
+    # R*nseg int4, each 256-B aligned)
     up = lambda x: (x + 255) // 256 * 256
-    assert L.pm_selective_scan_state_bytes(2, 8, 64, 16) == up(2 * 4 * 16 * 8 * 4) + 256 + 2 * up(2 * 1 * 16)
+    assert L.pm_selective_scan_state_bytes(2, 8, 64, 16) == (up(2 * 4 * 16 * 8 * 4) + 256 + up(2 * 1 * 4)
+                                                             + 2 * up(2 * 1 * 16))
 
 
 def test_pack_query_mode_and_capacity():
