@@ -202,6 +202,14 @@ PM_API pm_status pm_selective_scan_fwd(const void* u, const void* dt,
  * dA, dB, dC are required; dD, ddt_bias may be NULL.  All are overwritten.
  * states: the buffer filled by pm_selective_scan_fwd on the SAME inputs, or
  *   NULL to recompute it (then the workspace must also hold the states).
+ *   The chunk states are only read; the backward claims its work items
+ *   through the schedule counters kept in the same buffer (zeroed by the
+ *   forward, reset by the backward's last CTA), so one states buffer must
+ *   not be used by two backward calls running concurrently.  Enqueued
+ *   directly behind its forward kernel the backward is launched
+ *   programmatically (PDL): it starts on the SMs the forward's last CTAs
+ *   leave and waits per segment until the forward has released that
+ *   segment's states (PM_NO_PDL=1 in the environment disables the overlap).
  * workspace: >= pm_selective_scan_bwd_workspace(R, Dn, L, N, states==NULL)
  *   bytes of 16-byte aligned device memory. */
 PM_API size_t pm_selective_scan_bwd_workspace(int64_t R, int64_t Dn, int64_t L,
@@ -210,7 +218,7 @@ PM_API pm_status pm_selective_scan_bwd(const void* u, const void* dt,
                                 const float* A, const void* B, const void* C,
                                 const float* Dskip, const float* dt_bias,
                                 int32_t dt_softplus, const int32_t* pos,
-                                const float* states, const void* dy, void* du,
+                                float* states, const void* dy, void* du,
                                 void* ddt, float* dA, float* dB, float* dC,
                                 float* dD, float* ddt_bias, void* workspace,
                                 size_t ws_bytes, int64_t R, int64_t Dn,
@@ -274,7 +282,7 @@ PM_API pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt,
                                    const float* dt_bias, int32_t dt_softplus,
                                    int32_t zoh, const int32_t* pos,
                                    const void* z, const float* h0,
-                                   const float* states,
+                                   float* states,
                                    const void* dout, const float* dh_last,
                                    void* du, void* ddt, float* dA, float* dB,
                                    float* dC, float* dD, float* ddt_bias,

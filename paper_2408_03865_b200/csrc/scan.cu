@@ -137,7 +137,7 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
                                    const void* C, const float* Dskip, const float* dt_bias,
                                    int32_t dt_softplus, int32_t zoh, const int32_t* pos,
                                    const void* z,
-                                   const float* h0, const float* states, const void* dout,
+                                   const float* h0, float* states, const void* dout,
                                    const float* dh_last, void* du, void* ddt, float* dA,
                                    float* dB, float* dC, float* dD, float* ddt_bias, void* dz,
                                    float* dh0, void* workspace, size_t ws_bytes, int64_t R,
@@ -205,7 +205,7 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
 
 pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, const void* B,
                                 const void* C, const float* Dskip, const float* dt_bias,
-                                int32_t dt_softplus, const int32_t* pos, const float* states,
+                                int32_t dt_softplus, const int32_t* pos, float* states,
                                 const void* dy, void* du, void* ddt, float* dA, float* dB,
                                 float* dC, float* dD, float* ddt_bias, void* workspace,
                                 size_t ws_bytes, int64_t R, int64_t Dn, int64_t L, int32_t N,
