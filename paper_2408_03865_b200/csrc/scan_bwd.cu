@@ -59,8 +59,11 @@ struct BwdSmem {
   float sgz[kGate ? kChunk : 1][kBwdCh];  // dout * silu'(z) (gate only)
   float4 red[kBwdWarps][kRows][kRedStride];
   float4 xw[kChunk / 2][kBwdWarps][kRows][2];
-  float B[kChunk][N];
-  float C[kChunk][N];
+  // fp32 B/C of the chunk, [t][n]; rows padded by 4 floats (16-B aligned
+  // for the vector reads, 2-way instead of 16-way conflicts on the transpose)
+  static constexpr int kBS = N + 4;
+  float B[kChunk][kBS];
+  float C[kChunk][kBS];
   uint64_t bar;       // TMA completion barrier of the raw buffer
   unsigned hmask[1];  // head flags of the chunk (bit e = step cb + e)
   int s_red[kBwdWarps];
@@ -307,10 +310,13 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
         sm.sc[ii][cl] = make_float4(dl, active ? uu[i] : 0.f, active ? dyv : 0.f, sg);
       }
       if constexpr (kVec) {
-        for (int e = tid; e < N * kChunk; e += kBwdThreads) {
-          const int n = e % N, t = e / N;
+        // transpose [n][t] -> [t][n], two steps per thread (contiguous reads)
+        for (int e = tid; e < N * kChunk / 2; e += kBwdThreads) {
+          const int n = e / (kChunk / 2), t = 2 * (e % (kChunk / 2));
           sm.B[t][n] = IO<T>::cvt(sm.raw.B[n][t]);
+          sm.B[t + 1][n] = IO<T>::cvt(sm.raw.B[n][t + 1]);
           sm.C[t][n] = IO<T>::cvt(sm.raw.C[n][t]);
+          sm.C[t + 1][n] = IO<T>::cvt(sm.raw.C[n][t + 1]);
         }
         if (tid < 32) {
           const int t = cb + tid;
@@ -328,7 +334,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
           for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
         }
       } else {
-        stage_bc<T, N, kChunk, false>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.hmask,
+        stage_bc<T, N, kChunk, false, SM::kBS>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.hmask,
                                       a.h0 == nullptr);
         if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
           const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
@@ -553,7 +559,30 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
     else passes(std::false_type{});
     // ---- cross-warp sum of the chunk's dB/dC partials: one barrier ----
     __syncthreads();
-    {
+    if constexpr (NH % 4 == 0) {
+      // 4 consecutive outputs v..v+3 (same state half, same transpose row)
+      // are one float4 of every warp's partials: one vector sum per thread
+      constexpr int kV4 = 2 * N / 4;  // float4 groups per step
+      for (int e = tid; e < kChunk * kV4; e += kBwdThreads) {
+        const int s16 = e / kV4, v = 4 * (e % kV4);
+        const int t = cb + s16;
+        if (t >= c0 && t < c1) {
+          const int n = v < N ? v : v - N;
+          const int rh = n / NH;
+          const int kk = (v < N ? 0 : NH) + n % NH;
+          const int row = (s16 & 1) * kQ + kk / 4;
+          float4 acc = sm.xw[s16 >> 1][0][row][rh];
+#pragma unroll
+          for (int w = 1; w < kBwdWarps; ++w) {
+            const float4 q = sm.xw[s16 >> 1][w][row][rh];
+            const float2 lo = fadd2(make_float2(acc.x, acc.y), make_float2(q.x, q.y));
+            const float2 hi = fadd2(make_float2(acc.z, acc.w), make_float2(q.z, q.w));
+            acc = make_float4(lo.x, lo.y, hi.x, hi.y);
+          }
+          *reinterpret_cast<float4*>(ws_bc_r + (int64_t)t * (2 * N) + v) = acc;
+        }
+      }
+    } else {
       const float* xwf = reinterpret_cast<const float*>(&sm.xw[0][0][0][0]);
       constexpr int kWStride = kRows * 2 * 4;  // floats between warps
       for (int e = tid; e < kChunk * 2 * N; e += kBwdThreads) {

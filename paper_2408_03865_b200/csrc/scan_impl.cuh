@@ -115,10 +115,10 @@ struct ScanBwdArgs {
 // ---------------------------------------------------------------------------
 // Stage B, C (converted to fp32, time-major [t][n]) and head flags for the
 // time window [j0, j0 + W) of row r into shared memory.
-template <typename T, int N, int W, bool kVec>
+template <typename T, int N, int W, bool kVec, int S = N>  // S: row stride of sB/sC
 PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
                      const int32_t* __restrict__ pos_row, int L, int j0,
-                     float (*sB)[N], float (*sC)[N], unsigned* sMask, bool t0_head) {
+                     float (*sB)[S], float (*sC)[S], unsigned* sMask, bool t0_head) {
   static_assert(W % 8 == 0, "window must be a multiple of 8");
   for (int e = threadIdx.x; e < N * (W / 8); e += blockDim.x) {
     const int n = e % N, tb = (e / N) * 8;
