@@ -328,6 +328,8 @@ PM_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
 }
 PM_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 PM_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+template <int N>
+PM_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // ---------------------------------------------------------------- TMEM ----
 // Tensor memory used as per-thread scratch: a warp's 32 threads own the 32

@@ -2,6 +2,10 @@
 // P:202-205) and the segment schedule (plan + longest-first sort).
 #include "scan_impl.cuh"
 
+#ifndef PM_FWD_RING  // sub-blocks of u/dt in flight per thread (bf16 vector path); 1 = register prefetch
+#define PM_FWD_RING 2
+#endif
+
 namespace pm {
 
 // Work scheduling.  Segment lengths follow the sequence-length distribution
@@ -102,6 +106,10 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   __shared__ unsigned sMask[kTile / 32];
   __shared__ int s_red[kScanWarps];
   __shared__ int s_work;
+  constexpr bool kRing = kVec && sizeof(T) == 2 && PM_FWD_RING > 1;
+  constexpr int kRingDepth = kRing ? PM_FWD_RING : 1;
+  static_assert((kRingDepth & (kRingDepth - 1)) == 0, "ring depth: power of 2");
+  __shared__ __align__(16) uint4 ring[kRingDepth][2][kRing ? kScanThreads : 1];
 
   const int L = a.L, Dn = a.Dn;
   const int ndblk = (Dn + kScanThreads - 1) / kScanThreads;
@@ -183,8 +191,26 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   float sdl = 0.f;    // sum of delta over the segment (decay summary)
   bool anyh = false;  // a head inside the segment
   Raw8<T, kVec> pu, pt, pz;
-  pu.load(u_row, tb, L);
-  pt.load(dt_row, tb, L);
+  // bf16 vector path: u/dt of the next kRing-1 sub-blocks are in flight as
+  // per-thread cp.async copies into a shared ring (each thread reads back
+  // only its own slots: no barrier), deeper than one register block
+  auto ring_issue = [&](int t) {
+    if constexpr (kRing) {
+      if (t < s1) {
+        const int sl = (t >> 3) & (kRingDepth - 1);
+        cp_async16(&ring[sl][0][threadIdx.x], u_row + t, 16);
+        cp_async16(&ring[sl][1][threadIdx.x], dt_row + t, 16);
+      }
+      cp_async_commit();  // (empty past the segment: keeps the group count)
+    }
+  };
+  if constexpr (kRing) {
+#pragma unroll
+    for (int q = 0; q < kRingDepth - 1; ++q) ring_issue(tb + 8 * q);
+  } else {
+    pu.load(u_row, tb, L);
+    pt.load(dt_row, tb, L);
+  }
   if (kGate) pz.load(z_row, tb, L);
   int j0 = -1;
   unsigned long long hmask = 0ull;
@@ -199,12 +225,25 @@ scan_fwd_kernel(const ScanFwdArgs a) {
       hmask = (unsigned long long)sMask[0] | ((unsigned long long)sMask[1] << 32);
     }
     float uu[8], vv[8], yy[8], zz[8];
-    pu.unpack(uu);
-    pt.unpack(vv);
+    if constexpr (kRing) {
+      ring_issue(tb + 8 * (kRingDepth - 1));
+      cp_async_wait<kRingDepth - 1>();  // this sub-block's group has landed
+      const int sl = (tb >> 3) & (kRingDepth - 1);
+      Raw8<T, kVec> ru, rt;
+      ru.q = ring[sl][0][threadIdx.x];
+      rt.q = ring[sl][1][threadIdx.x];
+      ru.unpack(uu);
+      rt.unpack(vv);
+    } else {
+      pu.unpack(uu);
+      pt.unpack(vv);
+    }
     if (kGate) pz.unpack(zz);
     if (tb + 8 < s1) {
-      pu.load(u_row, tb + 8, L);
-      pt.load(dt_row, tb + 8, L);
+      if constexpr (!kRing) {
+        pu.load(u_row, tb + 8, L);
+        pt.load(dt_row, tb + 8, L);
+      }
       if (kGate) pz.load(z_row, tb + 8, L);
     }
     const int sb = tb - j0;
