@@ -694,28 +694,38 @@ scan_bwd_finalize_bc(const float* __restrict__ ws_bc, float* __restrict__ dB,
   }
 }
 
-// dA[d,n], dD[d], ddt_bias[d] = sum over (row, segment) partials.
+// dA[d,n], dD[d], ddt_bias[d] = sum over the R*nseg (row, segment) partials.
+// CTA = 32 consecutive outputs x 8 partial groups (group g sums partials
+// g, g+8, ...; loads coalesced across the outputs), combined in a fixed order.
 template <int N>
 __global__ void __launch_bounds__(256)
 scan_bwd_finalize_param(const float* __restrict__ ws, float* __restrict__ dA,
                         float* __restrict__ dD, float* __restrict__ ddtb, int nrs, int Dn) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)(N + 2) * Dn) return;
-  const int n = (int)(e / Dn), d = (int)(e % Dn);
-  // 8 independent partial sums (loads in flight), combined in a fixed order
-  float p[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  const float* src = ws + (int64_t)n * Dn + d;
-  const int64_t stride = (int64_t)(N + 2) * Dn;
-  int i = 0;
-  for (; i + 8 <= nrs; i += 8) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) p[k] += __ldcs(src + (i + k) * stride);
+  __shared__ float part[8][33];
+  const int j = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t nout = (int64_t)(N + 2) * Dn;
+  const int64_t e = (int64_t)blockIdx.x * 32 + j;
+  float acc = 0.f;
+  if (e < nout) {
+    float p0 = 0.f, p1 = 0.f;
+    int i = g;
+    for (; i + 8 < nrs; i += 16) {
+      p0 += __ldcs(ws + (int64_t)i * nout + e);
+      p1 += __ldcs(ws + (int64_t)(i + 8) * nout + e);
+    }
+    if (i < nrs) p0 += __ldcs(ws + (int64_t)i * nout + e);
+    acc = p0 + p1;
   }
-  for (; i < nrs; ++i) p[i & 7] += __ldcs(src + i * stride);
-  const float s = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-  if (n < N) dA[(int64_t)d * N + n] = s;
-  else if (n == N) { if (dD) dD[d] = s; }
-  else { if (ddtb) ddtb[d] = s; }
+  part[g][j] = acc;
+  __syncthreads();
+  if (g == 0 && e < nout) {
+    const float s = ((part[0][j] + part[1][j]) + (part[2][j] + part[3][j])) +
+                    ((part[4][j] + part[5][j]) + (part[6][j] + part[7][j]));
+    const int n = (int)(e / Dn), d = (int)(e % Dn);
+    if (n < N) dA[(int64_t)d * N + n] = s;
+    else if (n == N) { if (dD) dD[d] = s; }
+    else { if (ddtb) ddtb[d] = s; }
+  }
 }
 
 // ===========================================================================
@@ -781,7 +791,7 @@ pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, floa
   scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
   PM_LAUNCH_CHECK();
   const int64_t np = (int64_t)(N + 2) * a.Dn;
-  scan_bwd_finalize_param<N><<<(unsigned)((np + 255) / 256), 256, 0, s>>>(
+  scan_bwd_finalize_param<N><<<(unsigned)((np + 31) / 32), 256, 0, s>>>(
       a.ws_param, dA, dD, ddtb, a.R * a.nseg, a.Dn);
   PM_LAUNCH_CHECK();
   return PM_OK;
