@@ -769,7 +769,17 @@ pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = (a.done != nullptr && getenv("PM_NO_PDL") == nullptr) ? 1 : 0;
+    // Programmatic launch behind the forward pays when the forward is
+    // throughput-bound (its mean load per CTA slot is a good part of a row,
+    // so its tail is short and the backward fills it).  When a few long
+    // segments are the forward's critical path (mean load << L, e.g. the
+    // 130m config: 332 of 2048 steps) backward CTAs sharing those SMs slow
+    // that path down (measured +11 % step), so the launch stays serialized.
+    const int64_t fwd_slots = (int64_t)nsm * kFwdMinB;
+    const int64_t fwd_load = (int64_t)a.R * a.L * ((a.Dn + kScanThreads - 1) / kScanThreads) / fwd_slots;
+    const bool pdl = a.done != nullptr && getenv("PM_NO_PDL") == nullptr &&
+                     (getenv("PM_PDL") != nullptr || 10 * fwd_load >= 3 * (int64_t)a.L);
+    cfg.numAttrs = pdl ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return PM_ERR_CUDA;
   } else {
     kern<<<dim3(n_dblk_bwd(a.Dn), a.R, a.nseg), kBwdThreads, smem, s>>>(a);

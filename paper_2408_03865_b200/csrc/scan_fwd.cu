@@ -2,7 +2,7 @@
 // P:202-205) and the segment schedule (plan + longest-first sort).
 #include "scan_impl.cuh"
 
-#ifndef PM_FWD_RING  // sub-blocks of u/dt in flight per thread (bf16 vector path); 1 = register prefetch
+#ifndef PM_FWD_RING  // sub-blocks of u/dt in flight per thread (vector path); 1 = register prefetch
 #define PM_FWD_RING 2
 #endif
 
@@ -106,10 +106,11 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   __shared__ unsigned sMask[kTile / 32];
   __shared__ int s_red[kScanWarps];
   __shared__ int s_work;
-  constexpr bool kRing = kVec && sizeof(T) == 2 && PM_FWD_RING > 1;
+  constexpr bool kRing = kVec && PM_FWD_RING > 1;
   constexpr int kRingDepth = kRing ? PM_FWD_RING : 1;
+  constexpr int kQv = (int)sizeof(T) / 2;  // 16-byte pieces per 8-element block
   static_assert((kRingDepth & (kRingDepth - 1)) == 0, "ring depth: power of 2");
-  __shared__ __align__(16) uint4 ring[kRingDepth][2][kRing ? kScanThreads : 1];
+  __shared__ __align__(16) uint4 ring[kRingDepth][2][kQv][kRing ? kScanThreads : 1];
 
   const int L = a.L, Dn = a.Dn;
   const int ndblk = (Dn + kScanThreads - 1) / kScanThreads;
@@ -191,15 +192,20 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   float sdl = 0.f;    // sum of delta over the segment (decay summary)
   bool anyh = false;  // a head inside the segment
   Raw8<T, kVec> pu, pt, pz;
-  // bf16 vector path: u/dt of the next kRing-1 sub-blocks are in flight as
+  // vector path: u/dt of the next kRingDepth-1 sub-blocks are in flight as
   // per-thread cp.async copies into a shared ring (each thread reads back
   // only its own slots: no barrier), deeper than one register block
   auto ring_issue = [&](int t) {
     if constexpr (kRing) {
       if (t < s1) {
         const int sl = (t >> 3) & (kRingDepth - 1);
-        cp_async16(&ring[sl][0][threadIdx.x], u_row + t, 16);
-        cp_async16(&ring[sl][1][threadIdx.x], dt_row + t, 16);
+#pragma unroll
+        for (int q = 0; q < kQv; ++q) {  // fp32: the upper half may pass L (L % 8 == 4): zero-fill
+          const int tq = t + q * 4;
+          const int nb = tq < L ? 16 : 0;
+          cp_async16(&ring[sl][0][q][threadIdx.x], nb ? u_row + tq : u_row, nb);
+          cp_async16(&ring[sl][1][q][threadIdx.x], nb ? dt_row + tq : dt_row, nb);
+        }
       }
       cp_async_commit();  // (empty past the segment: keeps the group count)
     }
@@ -229,11 +235,21 @@ scan_fwd_kernel(const ScanFwdArgs a) {
       ring_issue(tb + 8 * (kRingDepth - 1));
       cp_async_wait<kRingDepth - 1>();  // this sub-block's group has landed
       const int sl = (tb >> 3) & (kRingDepth - 1);
-      Raw8<T, kVec> ru, rt;
-      ru.q = ring[sl][0][threadIdx.x];
-      rt.q = ring[sl][1][threadIdx.x];
-      ru.unpack(uu);
-      rt.unpack(vv);
+      if constexpr (sizeof(T) == 2) {
+        Raw8<T, kVec> ru, rt;
+        ru.q = ring[sl][0][0][threadIdx.x];
+        rt.q = ring[sl][1][0][threadIdx.x];
+        ru.unpack(uu);
+        rt.unpack(vv);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const float4 a4 = *reinterpret_cast<const float4*>(&ring[sl][0][q][threadIdx.x]);
+          const float4 b4 = *reinterpret_cast<const float4*>(&ring[sl][1][q][threadIdx.x]);
+          uu[4 * q] = a4.x; uu[4 * q + 1] = a4.y; uu[4 * q + 2] = a4.z; uu[4 * q + 3] = a4.w;
+          vv[4 * q] = b4.x; vv[4 * q + 1] = b4.y; vv[4 * q + 2] = b4.z; vv[4 * q + 3] = b4.w;
+        }
+      }
     } else {
       pu.unpack(uu);
       pt.unpack(vv);
