@@ -176,7 +176,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
         // buffer not written by the forward must not hang the GPU)
         const int4 it = a.items[w / ndblk];
         const int* dp = a.done + it.x * a.nseg + it.y;
-        const int need = (a.Dn + kScanThreads - 1) / kScanThreads;  // fwd channel blocks
+        const int need = a.fwd_ndblk;  // forward channel blocks of the segment
         for (int spin = 0; spin < (1 << 22) && ld_acquire(dp) < need; ++spin) __nanosleep(256);
         fence_proxy_async_global();  // the states are read by TMA (async proxy)
       }
@@ -775,10 +775,8 @@ pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
     // segments are the forward's critical path (mean load << L, e.g. the
     // 130m config: 332 of 2048 steps) backward CTAs sharing those SMs slow
     // that path down (measured +11 % step), so the launch stays serialized.
-    const int64_t fwd_slots = (int64_t)nsm * kFwdMinB;
-    const int64_t fwd_load = (int64_t)a.R * a.L * ((a.Dn + kScanThreads - 1) / kScanThreads) / fwd_slots;
     const bool pdl = a.done != nullptr && getenv("PM_NO_PDL") == nullptr &&
-                     (getenv("PM_PDL") != nullptr || 10 * fwd_load >= 3 * (int64_t)a.L);
+                     (getenv("PM_PDL") != nullptr || fwd_throughput_bound(a.R, a.L, a.Dn));
     cfg.numAttrs = pdl ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return PM_ERR_CUDA;
   } else {

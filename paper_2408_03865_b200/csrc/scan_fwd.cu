@@ -98,9 +98,15 @@ __global__ void __launch_bounds__(1024) seg_sort_kernel(const int4* __restrict__
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
-template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh>
+// S threads per channel (S = 1: all N states in one thread; S > 1, for
+// latency-bound launches: N/S states each, y summed over the S lanes by
+// shuffle -- a few long segments then run S times as many warps).
+template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh, int S = 1>
 __global__ void __launch_bounds__(kScanThreads, MinB)
 scan_fwd_kernel(const ScanFwdArgs a) {
+  constexpr int kCh = kScanThreads / S;  // channels per CTA
+  constexpr int NS = N / S;              // states per thread
+  static_assert(NS % 2 == 0, "states are processed in pairs");
   __shared__ __align__(16) float sB[kTile][N];
   __shared__ __align__(16) float sC[kTile][N];
   __shared__ unsigned sMask[kTile / 32];
@@ -113,7 +119,9 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   __shared__ __align__(16) uint4 ring[kRingDepth][2][kQv][kRing ? kScanThreads : 1];
 
   const int L = a.L, Dn = a.Dn;
-  const int ndblk = (Dn + kScanThreads - 1) / kScanThreads;
+  const int ndblk = (Dn + kCh - 1) / kCh;
+  const int part = S > 1 ? (int)threadIdx.x % S : 0;
+  const int n0 = part * NS;  // first state of this thread
   // the backward (launched programmatically behind this kernel) takes the SM
   // slots this kernel's CTAs leave; it waits per segment on a.done
   pdl_launch_dependents();
@@ -145,7 +153,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     segment_bounds(a.pos + (int64_t)r * L, L, blockIdx.z, a.nseg, s_red, s0, s1);
   }
   if (s0 >= s1) continue;
-  const int d_raw = dblk * kScanThreads + threadIdx.x;
+  const int d_raw = dblk * kCh + (int)threadIdx.x / S;
   const bool active = d_raw < Dn;
   const int d = active ? d_raw : Dn - 1;
   const int32_t* pos_row = a.pos + (int64_t)r * L;
@@ -159,27 +167,27 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   const T* z_row = kGate ? static_cast<const T*>(a.z) + lane : nullptr;
 
   // states are processed in pairs with packed fp32x2 arithmetic (FFMA2)
-  constexpr int NP = N / 2;
+  constexpr int NP = NS / 2;
   float2 A2[NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p)
-    A2[p] = make_float2(__ldg(a.A + (int64_t)d * N + 2 * p) * kLog2e,
-                        __ldg(a.A + (int64_t)d * N + 2 * p + 1) * kLog2e);
+    A2[p] = make_float2(__ldg(a.A + (int64_t)d * N + n0 + 2 * p) * kLog2e,
+                        __ldg(a.A + (int64_t)d * N + n0 + 2 * p + 1) * kLog2e);
   float2 invA[kZoh ? NP : 1];  // 1/A for the ZOH factor (inf at A = 0: series branch)
   if constexpr (kZoh) {
 #pragma unroll
     for (int p = 0; p < NP; ++p)
-      invA[p] = make_float2(1.f / __ldg(a.A + (int64_t)d * N + 2 * p),
-                            1.f / __ldg(a.A + (int64_t)d * N + 2 * p + 1));
+      invA[p] = make_float2(1.f / __ldg(a.A + (int64_t)d * N + n0 + 2 * p),
+                            1.f / __ldg(a.A + (int64_t)d * N + n0 + 2 * p + 1));
   }
-  const float Dd = a.Dskip ? __ldg(a.Dskip + d) : 0.f;
+  const float Dd = (a.Dskip && part == 0) ? __ldg(a.Dskip + d) : 0.f;  // skip term once per channel
   const float bias = a.dt_bias ? __ldg(a.dt_bias + d) : 0.f;
 
   float2 h[NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) h[p] = make_float2(0.f, 0.f);
   if (s0 == 0 && a.h0 != nullptr) {  // NEXT-2: state carried into the row
-    const float* hp = a.h0 + ((int64_t)r * Dn + d) * N;
+    const float* hp = a.h0 + ((int64_t)r * Dn + d) * N + n0;
 #pragma unroll
     for (int p = 0; p < NP; ++p) h[p] = make_float2(__ldg(hp + 2 * p), __ldg(hp + 2 * p + 1));
   }
@@ -265,7 +273,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     const int sb = tb - j0;
     // checkpoint = state before step tb (only step i == 0 can be a multiple of kChunk)
     if (a.states != nullptr && (tb % kChunk) == 0 && tb >= s0 && active) {
-      float* st = a.states + (((int64_t)r * a.nchunk + tb / kChunk) * N) * Dn + d;
+      float* st = a.states + (((int64_t)r * a.nchunk + tb / kChunk) * N + n0) * Dn + d;
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         st[(int64_t)(2 * p) * Dn] = h[p].x;
@@ -293,8 +301,8 @@ scan_fwd_kernel(const ScanFwdArgs a) {
         if (!kFull && (t < s0 || t >= s1)) continue;  // CTA-uniform
         const float delta = dls[i];
         const float2 dux2 = f2(delta * uu[i]), dl2 = f2(delta);
-        const float2* Bt = reinterpret_cast<const float2*>(sB[sb + i]);
-        const float2* Ct = reinterpret_cast<const float2*>(sC[sb + i]);
+        const float2* Bt = reinterpret_cast<const float2*>(sB[sb + i] + n0);
+        const float2* Ct = reinterpret_cast<const float2*>(sC[sb + i] + n0);
         if constexpr (kZoh) {  // B-bar u = f(z) delta B u (Eq 2b); abar needed at heads too
           const bool head = !kNoHead && ((hmask >> (sb + i)) & 1ull);
           const float2 u2 = f2(uu[i]);
@@ -319,7 +327,10 @@ scan_fwd_kernel(const ScanFwdArgs a) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) yp[p & 1] = ffma2(Ct[p], h[p], yp[p & 1]);
         const float2 ys = fadd2(yp[0], yp[1]);
-        yy[i] = ys.x + ys.y;
+        float yv = ys.x + ys.y;
+#pragma unroll
+        for (int o = 1; o < S; o <<= 1) yv += __shfl_xor_sync(0xffffffffu, yv, o);  // CTA-uniform path
+        yy[i] = yv;
         if (kGate) yy[i] *= zz[i] * sigmoidf_fast(zz[i]);  // out = y * silu(z)
       }
     };
@@ -329,7 +340,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     } else {
       block(std::false_type{}, std::false_type{});
     }
-    if (active && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
+    if (active && part == 0 && y_row != nullptr) store8<T, kVec>(y_row, tb, s0, s1, yy);
     if (a.decay != nullptr) {  // NEXT-2 row summary: sum of delta, any head
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -343,7 +354,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   if (s1 == L && a.decay != nullptr && active) {
     // d h_last / d h0 = prod_t abar_t = exp(A sum_t delta_t) when no slot of
     // the row is a head (the whole row is then one segment), else 0
-    float* dp = a.decay + ((int64_t)r * Dn + d) * N;
+    float* dp = a.decay + ((int64_t)r * Dn + d) * N + n0;
     const bool live = s0 == 0 && !anyh;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -352,7 +363,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     }
   }
   if (s1 == L && a.h_last != nullptr && active) {  // state after the row's last step
-    float* hp = a.h_last + ((int64_t)r * Dn + d) * N;
+    float* hp = a.h_last + ((int64_t)r * Dn + d) * N + n0;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
       hp[2 * p] = h[p].x;
@@ -381,11 +392,12 @@ int persistent_grid(K kern, int threads, size_t smem, int64_t items) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(g, items));
 }
 
-template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh>
+template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh, int S = 1>
 void fwd_go(const ScanFwdArgs& a, cudaStream_t s) {
-  auto kern = scan_fwd_kernel<T, N, kVec, MinB, kGate, kZoh>;
+  auto kern = scan_fwd_kernel<T, N, kVec, MinB, kGate, kZoh, S>;
   if (a.items != nullptr) {
-    const int g = persistent_grid(kern, kScanThreads, 0, (int64_t)a.n_items * n_dblk(a.Dn));
+    const int64_t nd = (a.Dn + kScanThreads / S - 1) / (kScanThreads / S);
+    const int g = persistent_grid(kern, kScanThreads, 0, (int64_t)a.n_items * nd);
     kern<<<g, kScanThreads, 0, s>>>(a);
   } else {
     kern<<<dim3(n_dblk(a.Dn), a.R, a.nseg), kScanThreads, 0, s>>>(a);
@@ -409,6 +421,8 @@ pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
     else fwd_go<T, N, kVec, 3, false, true>(a, s);
   } else {
     if (a.z != nullptr) fwd_go<T, N, kVec, kFwdMinB, true, false>(a, s);
+    else if (a.items != nullptr && fwd_split(a.R, a.L, a.Dn, N) > 1)
+      fwd_go<T, N, kVec, kFwdMinB, false, false, kFwdSplit<N>>(a, s);
     else fwd_go<T, N, kVec, kFwdMinB, false, false>(a, s);
   }
   PM_LAUNCH_CHECK();

@@ -96,7 +96,7 @@ struct ScanBwdArgs {
   float* ws_param;  // (R*nseg, N+2, Dn)
   const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
   int* counter;       // counters[1] of the schedule: work counter; counter[1]: CTAs exited
-  const int* done;    // the fwd's per-segment done counts (wait for n_dblk(Dn) each)
+  const int* done;    // the fwd's per-segment done counts (wait for fwd_ndblk each)
   int n_items;
   int R, Dn, L, nseg, nchunk, softplus;
   const void* z;        // NEXT-1 gate (R,Dn,L) or NULL; dy is then d(out)
@@ -105,6 +105,7 @@ struct ScanBwdArgs {
   void* dz;             // (R,Dn,L) when z != NULL
   float* dh0;           // (R,Dn,N) when h0 != NULL
   int zoh;              // NEXT-4: Eq 2b discretisation of B-bar (else Euler, Q1)
+  int fwd_ndblk = 1;    // forward channel blocks per segment (set by the host)
   // TMA descriptors of the per-chunk inputs (vector path; use_tma = 0 falls
   // back to cp.async): (L, Dn, R) u/dt/dy/z, (L, N, R) B/C, (L, R) pos,
   // (Dn, N, nchunk, R) states
@@ -151,6 +152,34 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
 inline int n_chunks(int64_t L) { return (int)((L + kChunk - 1) / kChunk); }
 inline int n_dblk(int64_t Dn) { return (int)((Dn + kScanThreads - 1) / kScanThreads); }
 inline int n_dblk_bwd(int64_t Dn) { return (int)((Dn + kBwdCh - 1) / kBwdCh); }
+
+// Forward launch shape.  Throughput-bound when the mean load per CTA slot
+// (R*L*ceil(Dn/128) step-items over nsm*kFwdMinB slots) is >= 0.3 L: one
+// thread per channel (S = 1) and the backward launched programmatically
+// behind it.  Otherwise a few long segments are the critical path: S =
+// kFwdSplit threads per channel (N/S states each) and a serialized backward.
+// PM_FWD_SPLIT=1|S overrides the choice (A/B).
+template <int N> constexpr int kFwdSplit = N >= 8 ? 4 : 2;
+inline int sm_count() {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return nsm;
+}
+inline bool fwd_throughput_bound(int64_t R, int64_t L, int64_t Dn) {
+  const int64_t load = R * L * ((Dn + kScanThreads - 1) / kScanThreads) / ((int64_t)sm_count() * kFwdMinB);
+  return 10 * load >= 3 * L;
+}
+inline int fwd_split(int64_t R, int64_t L, int64_t Dn, int N) {
+  const int sp = N >= 8 ? 4 : 2;
+  if (const char* e = getenv("PM_FWD_SPLIT")) return atoi(e) > 1 ? sp : 1;
+  return fwd_throughput_bound(R, L, Dn) ? 1 : sp;
+}
+// forward channel blocks per segment (the backward waits for that many)
+inline int fwd_ndblk(int64_t R, int64_t L, int64_t Dn, int N) {
+  const int ch = kScanThreads / fwd_split(R, L, Dn, N);
+  return (int)((Dn + ch - 1) / ch);
+}
 
 // Segments per row: nominal cut every 256 steps (cuts snap to heads, so with
 // the paper's length distribution a segment is ~one sequence), <= 64.

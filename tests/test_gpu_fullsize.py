@@ -53,7 +53,7 @@ def row_np(t, r):
 
 
 @pytest.mark.parametrize("name,R", [("1.4b", 8), ("2.8b-16k", 8)])
-def test_fullsize_sampled_rows(name, R):
+def test_fullsize_sampled_rows(monkeypatch, name, R):
     cfg = workload.CONFIGS[name]
     io = cfg.dtype
     pos_np, valid, T, P = build(cfg, R)
@@ -78,10 +78,14 @@ def test_fullsize_sampled_rows(name, R):
     # (b) properties of the full launch: dD[d] = sum_{r,t} dy * u
     dD = (T["dy"].double() * out["u"].double()).sum(dim=(0, 2)).cpu().numpy()
     assert rel_err(to_np(out["dD"]), dD) <= TOL[(io, "bwd")]
-    # (a) single-row launch: parameter gradients vs the oracle
+    # (a) single-row launch: parameter gradients vs the oracle.  One row
+    # alone is a latency-bound launch, for which the library would split
+    # each channel's states over 4 lanes (y then sums in another order);
+    # pin the full launch's shape so the row's outputs must match bit for bit
+    monkeypatch.setenv("PM_FWD_SPLIT", "1")
     T1 = {k: v[r:r + 1].contiguous() for k, v in T.items()}
     o1 = chain(pos[r:r + 1].contiguous(), T1, P)
-    for k in ("du", "ddt", "dB", "dC", "y", "u"):  # same row, different launch shape
+    for k in ("du", "ddt", "dB", "dC", "y", "u"):  # same row, other rows absent
         assert torch.equal(o1[k][0], out[k][r]), k
     for k, ref in (("dA", g["dA"]), ("dD", g["dD"]), ("ddt_bias", g["ddt_bias"])):
         e = rel_err(to_np(o1[k]), ref)

@@ -101,6 +101,20 @@ def test_chain_state_and_width(io, N, K):
     check_chain(pos, T, P, out, io)
 
 
+@pytest.mark.parametrize("split", ["1", "4"])
+@pytest.mark.parametrize("io,N,kind", [("f32", 16, "edges"), ("bf16", 16, "random"),
+                                       ("bf16", 8, "short"), ("f32", 4, "heads")])
+def test_fwd_launch_shapes(monkeypatch, split, io, N, kind):
+    """Both forward launch shapes (one thread per channel, and N/S states per
+    thread with S lanes per channel for latency-bound launches; the library
+    picks by load, PM_FWD_SPLIT forces one) against the oracle, with the
+    backward waiting on the matching number of forward channel blocks."""
+    monkeypatch.setenv("PM_FWD_SPLIT", split)
+    rows, pos, valid, T, P = problem(3, 200, 1024, N, 4, kind, io, seed=100 + N)
+    out = run_chain(pos, T, P)
+    check_chain(pos, T, P, out, io)
+
+
 @pytest.mark.parametrize("L", [1, 7, 13, 100, 1001, 2051])
 def test_ragged_lengths_scalar_path(L):
     """L not a multiple of 8 takes the scalar (unaligned) path."""
