@@ -198,7 +198,6 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
   // TMA for the per-chunk inputs when the vector path applies (row strides
   // are then multiples of 16 bytes); cp.async otherwise.  PM_NO_TMA=1 forces
   // cp.async (A/B measurements).
-  a.fwd_ndblk = fwd_ndblk(R, L, Dn, N);
   a.use_tma = vec && Dn % 4 == 0 && getenv("PM_NO_TMA") == nullptr &&
               encode_bwd_maps(a, (int)N, io) ? 1 : 0;
   return run_scan_bwd(a, (int)N, vec, io, dA, dB, dC, dD, ddt_bias, s);

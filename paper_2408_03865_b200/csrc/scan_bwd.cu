@@ -176,7 +176,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
         // buffer not written by the forward must not hang the GPU)
         const int4 it = a.items[w / ndblk];
         const int* dp = a.done + it.x * a.nseg + it.y;
-        const int need = a.fwd_ndblk;  // forward channel blocks of the segment
+        const int need = a.Dn;  // every channel of the segment released by the forward
         for (int spin = 0; spin < (1 << 22) && ld_acquire(dp) < need; ++spin) __nanosleep(256);
         fence_proxy_async_global();  // the states are read by TMA (async proxy)
       }

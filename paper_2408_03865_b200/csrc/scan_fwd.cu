@@ -133,8 +133,11 @@ scan_fwd_kernel(const ScanFwdArgs a) {
       // release the finished item's segment (thread 0 re-reads its item
       // rather than keeping it in a register across the item)
       if (iter > 0) {
+        // (counted in channels, so the backward's completion test, == Dn,
+        // does not depend on this launch's channel-block width)
         const int4 pv = a.items[s_work / ndblk];
-        red_release_add(a.done + pv.x * a.nseg + pv.y, 1);
+        const int pb = s_work % ndblk;
+        red_release_add(a.done + pv.x * a.nseg + pv.y, min(kCh, Dn - pb * kCh));
       }
       s_work = atomicAdd(a.counter, 1);
     }

@@ -96,7 +96,7 @@ struct ScanBwdArgs {
   float* ws_param;  // (R*nseg, N+2, Dn)
   const int4* items;  // length-sorted segment list {r, k, s0, s1} (NULL: grid mode)
   int* counter;       // counters[1] of the schedule: work counter; counter[1]: CTAs exited
-  const int* done;    // the fwd's per-segment done counts (wait for fwd_ndblk each)
+  const int* done;    // the fwd's per-segment released channel counts (complete at Dn)
   int n_items;
   int R, Dn, L, nseg, nchunk, softplus;
   const void* z;        // NEXT-1 gate (R,Dn,L) or NULL; dy is then d(out)
@@ -105,7 +105,6 @@ struct ScanBwdArgs {
   void* dz;             // (R,Dn,L) when z != NULL
   float* dh0;           // (R,Dn,N) when h0 != NULL
   int zoh;              // NEXT-4: Eq 2b discretisation of B-bar (else Euler, Q1)
-  int fwd_ndblk = 1;    // forward channel blocks per segment (set by the host)
   // TMA descriptors of the per-chunk inputs (vector path; use_tma = 0 falls
   // back to cp.async): (L, Dn, R) u/dt/dy/z, (L, N, R) B/C, (L, R) pos,
   // (Dn, N, nchunk, R) states
@@ -175,11 +174,6 @@ inline int fwd_split(int64_t R, int64_t L, int64_t Dn, int N) {
   if (const char* e = getenv("PM_FWD_SPLIT")) return atoi(e) > 1 ? sp : 1;
   return fwd_throughput_bound(R, L, Dn) ? 1 : sp;
 }
-// forward channel blocks per segment (the backward waits for that many)
-inline int fwd_ndblk(int64_t R, int64_t L, int64_t Dn, int N) {
-  const int ch = kScanThreads / fwd_split(R, L, Dn, N);
-  return (int)((Dn + ch - 1) / ch);
-}
 
 // Segments per row: nominal cut every 256 steps (cuts snap to heads, so with
 // the paper's length distribution a segment is ~one sequence), <= 64.
@@ -190,8 +184,8 @@ inline int n_seg(int64_t L) { return (int)std::max<int64_t>(1, std::min<int64_t>
 // schedule; the bwd reuses it).  counters[0]: fwd work counter; [1]: bwd
 // work counter; [2]: bwd CTAs exited (the last one resets [1] and [2], so the
 // bwd needs no memset of its own and can launch programmatically right
-// behind the fwd).  done[r*nseg+k]: fwd channel blocks finished on segment
-// (r,k) -- a bwd item starts once its segment's count is complete.
+// behind the fwd).  done[r*nseg+k]: fwd channels finished on segment
+// (r,k) -- a bwd item starts once its segment's count reaches Dn.
 inline size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
 inline size_t states_f32_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
   return (size_t)R * n_chunks(L) * N * Dn * sizeof(float);
