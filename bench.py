@@ -161,6 +161,16 @@ def build_layout(cfg, total_rows):
     return lens[keep], row[keep], off[keep]
 
 
+def config_dict(cfg, world, pad):
+    """The workload description both arms print (native and --impl reference)."""
+    return {"workload": f"{cfg.name}: Mamba layer shape R={cfg.R} rows/GPU x "
+                        f"L={cfg.L}, d_inner={cfg.Dn}, d_state={cfg.N}, conv={cfg.K}",
+            "global_rows": cfg.R * world, "io_dtype": cfg.dtype,
+            "lengths": "lognormal [57,2048] mean~646 (P:246), FIFO-packed (P:273)",
+            "padding_rate": pad, "parallelism": f"dp{world} (row-sharded)",
+            "l2": "inputs larger than L2 (256 MiB per (R,Dn,L) tensor)"}
+
+
 def packing_report(cfg, n=20000):
     """NEXT-3 (sec 5 E6): padding rate of FIFO-seal vs the greedy
     sort-then-pack planner vs pad-to-max on n sequences of the workload's
@@ -350,8 +360,7 @@ def run_reference(args, cfg):
            "warmup": args.warmup, "ms_per_step": el * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"{cfg.name}: R={cfg.R} L={cfg.L} Dn={cfg.Dn} N={cfg.N} "
-                                  f"K={cfg.K}", "io": cfg.dtype},
+           "config": config_dict(cfg, world, 1.0 - float(np.sum(lens)) / (cfg.R * cfg.L)),
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": orc.num_threads(),
                             "kind": "oracle", "sample": sample},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -524,13 +533,8 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": cfg.dtype, "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: Mamba layer shape R={cfg.R} rows/GPU x "
-                                   f"L={cfg.L}, d_inner={cfg.Dn}, d_state={cfg.N}, conv={cfg.K}",
-                       "global_rows": cfg.R * world, "io_dtype": cfg.dtype,
-                       "lengths": "lognormal [57,2048] mean~646 (P:246), FIFO-packed (P:273)",
-                       "padding_rate": D["pad"], "packing": packing_report(cfg),
-                       "parallelism": f"dp{world} (row-sharded)",
-                       "l2": "inputs larger than L2 (256 MiB per (R,Dn,L) tensor)"},
+            "config": config_dict(cfg, world, D["pad"]),
+            "packing": packing_report(cfg),
             "real_tokens_per_s": value * (1 - D["pad"]),
             "hbm_frac_step": hbm_frac_step,
             "hbm_peak_gbs": peaks["hbm_gbs"], "peak_source": peaks["source"],
