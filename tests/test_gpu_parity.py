@@ -282,3 +282,19 @@ def test_tma_and_cp_async_staging_agree(monkeypatch):
     b = run_chain(pos, T, P)
     for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dx", "dw", "db"):
         assert torch.equal(a[k], b[k]), k
+
+
+def test_programmatic_launch_over_split_forward_is_bit_identical(monkeypatch):
+    """Forcing the programmatic bwd launch (PM_PDL) onto a latency-bound
+    launch, where the forward splits each channel over 4 lanes: the bwd waits
+    for every channel of a segment to be released (counted in channels, not
+    blocks), so the results equal the serialized launch bit for bit."""
+    rows, pos, valid, T, P = problem(3, 200, 1024, 16, 4, "random", "bf16", seed=77)
+    monkeypatch.setenv("PM_NO_PDL", "1")
+    ref = run_chain(pos, T, P)
+    monkeypatch.delenv("PM_NO_PDL")
+    monkeypatch.setenv("PM_PDL", "1")
+    for _ in range(3):
+        got = run_chain(pos, T, P)
+        for k in ("y", "du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dx"):
+            assert torch.equal(got[k], ref[k]), k
