@@ -3,6 +3,9 @@
 // P:224) and its deterministic finalize kernels.
 #include "scan_impl.cuh"
 
+#ifndef PM_BWD_AUNROLL  // steps unrolled per iteration of the full-chunk forward recompute (pass A)
+#define PM_BWD_AUNROLL 16
+#endif
 #ifndef PM_BWD_UNROLL  // 2-step rounds unrolled per iteration of the full-chunk reverse pass
 #define PM_BWD_UNROLL 4
 #endif
@@ -10,6 +13,7 @@
 namespace pm {
 
 constexpr int kBwdUnroll = PM_BWD_UNROLL;
+constexpr int kBwdAUnroll = PM_BWD_AUNROLL;
 
 // ---------------------------------------------------------------------------
 // backward
@@ -386,7 +390,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
       }
     };
     if constexpr (kFull) {
-#pragma unroll
+#pragma unroll kBwdAUnroll
       for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
     } else {
 #pragma unroll 1
