@@ -36,9 +36,12 @@ import workload  # noqa: E402
 METRIC = "scan+conv fwd+bwd packed tokens/s (1.4B shape) at 1/2/4/8 B200; % HBM peak"
 UNIT = "tokens/s"
 
-# minimal algorithmic lane-ops per (t, d, n) element of the scan kernels and
-# per (t, d) of the conv kernels; 1 MUFU ex2 counted as 1
-ALU_OPS = {"scan_fwd": 5, "scan_bwd": 15}
+# Algorithmic operation counts of the scan kernels (SURVEY.md §8(d)
+# "Algorithmic ops per slot"), per (t, d, n) element: FP32 lane-ops (an FFMA
+# counts as one) and MUFU ops (ex2; the softplus' 2 (fwd) / 3 (bwd) per (t, d)
+# spread over the N states).
+FP32_OPS = {"scan_fwd": 4.0, "scan_bwd": 20.0}
+MUFU_OPS = {"scan_fwd": lambda N: 1.0 + 2.0 / N, "scan_bwd": lambda N: 1.0 + 3.0 / N}
 
 
 def algo_bytes(Dn, N, isz):
@@ -52,13 +55,20 @@ def algo_bytes(Dn, N, isz):
 
 
 def load_peaks():
+    """HBM peak from MEASURED_PEAKS.json (driver-measured copy bandwidth);
+    the scan's issue roofs from the guide's unit counts at the measured max
+    SM clock: 148 SMs x 128 FP32 lanes (FFMA2 issues 2 per lane; counted as
+    the scalar rate) and 148 x 16 MUFU lanes."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    mhz, hbm, src = 1965.0, 6650.0, "fallback (B200_PROFILING.md)"
     if os.path.exists(path):
         with open(path) as f:
             p = json.load(f)
-        return dict(hbm_gbs=float(p["hbm_gbs"]), sm_max_mhz=float(p.get("sm_max_mhz", 1965.0)),
-                    source="measured")
-    return dict(hbm_gbs=6650.0, sm_max_mhz=1965.0, source="fallback")
+        hbm, mhz, src = float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    return dict(hbm_gbs=hbm, sm_max_mhz=mhz, source=src,
+                fp32_tops=148 * 128 * mhz * 1e6 / 1e12, mufu_tops=148 * 16 * mhz * 1e6 / 1e12,
+                alu_source=f"148 SMs x (128 FP32 | 16 MUFU) lanes/clk x {mhz:.0f} MHz "
+                           "(guide unit counts at MEASURED_PEAKS sm_max_mhz)")
 
 
 # ---------------------------------------------------------------------------
@@ -234,18 +244,34 @@ class Step:
                                    dtype=torch.uint8, device=dev)
         self.events = None
 
-    def kernels(self, ev=None, inp=None, dx=None, pg=None, split=True):
+    def new_outs(self):
+        """A second set of the step's outputs (double-buffered e2e)."""
+        torch, T, cfg = self.torch, self.D["T"], self.cfg
+        f32 = dict(dtype=torch.float32, device=self.dx.device)
+        return dict(y=torch.empty_like(T["x"]), ddt=torch.empty_like(T["x"]),
+                    dB=torch.empty((cfg.R, cfg.N, cfg.L), **f32),
+                    dC=torch.empty((cfg.R, cfg.N, cfg.L), **f32), dx=torch.empty_like(T["x"]),
+                    pg=self.D["ParamGrads"](torch, cfg.Dn, cfg.N, cfg.K, self.dx.device))
+
+    def outs(self):
+        return dict(y=self.y, ddt=self.g["ddt"], dB=self.g["dB"], dC=self.g["dC"], dx=self.dx,
+                    pg=self.pg)
+
+    def kernels(self, ev=None, inp=None, outs=None, split=False):
         """One step on inputs ``inp`` (dict x, dt, B, C, dy, pos; default the
-        resident set), writing dx and the param-grad buffer ``pg``.  With
-        ``split=False`` no event sits between the scan fwd and bwd launches,
-        so the bwd launches programmatically behind the fwd and fills the SM
-        slots of its tail (ev[2] is then not recorded)."""
+        resident set), writing the step's outputs ``outs`` (y, ddt, dB, dC,
+        dx and the param-grad buffer pg; default the resident set).  With
+        ``split=False`` the scan fwd and bwd run as ONE library call
+        (pm_selective_scan_fwd_bwd), so the bwd launches programmatically
+        behind the fwd and fills the SM slots of its tail (ev[2] is then not
+        recorded); ``split=True`` calls them separately (plain launches)."""
         pm, P = self.pm, self.D["P"]
         T = inp if inp is not None else self.D["T"]
         pos = T["pos"] if inp is not None else self.D["pos"]
-        dx = self.dx if dx is None else dx
-        pg = self.pg if pg is None else pg
-        g = dict(self.g, dA=pg["dA"], dD=pg["dD"], ddt_bias=pg["ddt_bias"])
+        o = outs if outs is not None else self.outs()
+        pg = o["pg"]
+        g = dict(self.g, ddt=o["ddt"], dB=o["dB"], dC=o["dC"], dA=pg["dA"], dD=pg["dD"],
+                 ddt_bias=pg["ddt_bias"])
 
         def mark(i):
             if ev is not None and (split or i != 2):
@@ -253,14 +279,19 @@ class Step:
         mark(0)
         pm.pm_causal_conv1d_fwd(T["x"], P["w"], P["bias"], pos, out=self.u, silu=True)
         mark(1)
-        pm.pm_selective_scan_fwd(self.u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
-                                 pos, y=self.y, states=self.states)
-        mark(2)
-        pm.pm_selective_scan_bwd(self.u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
-                                 pos, T["dy"], states=self.states, out=g,
-                                 workspace=self.ws_scan)
+        if split:
+            pm.pm_selective_scan_fwd(self.u, T["dt"], P["A"], T["B"], T["C"], P["D"],
+                                     P["dt_bias"], pos, y=o["y"], states=self.states)
+            mark(2)
+            pm.pm_selective_scan_bwd(self.u, T["dt"], P["A"], T["B"], T["C"], P["D"],
+                                     P["dt_bias"], pos, T["dy"], states=self.states, out=g,
+                                     workspace=self.ws_scan)
+        else:  # one call: the bwd launches programmatically behind the library's own fwd
+            pm.pm_selective_scan_fwd_bwd(self.u, T["dt"], P["A"], T["B"], T["C"], P["D"],
+                                         P["dt_bias"], pos, T["dy"], self.states, out=o["y"],
+                                         grads=g, workspace=self.ws_scan)
         mark(3)
-        pm.pm_causal_conv1d_bwd(T["x"], P["w"], P["bias"], pos, g["du"], dx=dx,
+        pm.pm_causal_conv1d_bwd(T["x"], P["w"], P["bias"], pos, g["du"], dx=o["dx"],
                                 dw=pg["dw"], dbias=pg["db"], workspace=self.ws_conv)
         mark(4)
         if self.world > 1:
@@ -331,8 +362,24 @@ def cpu_baseline(torch, cfg, target_s=15.0):
     oracle_step(orc, cfg, s)
     dt = time.perf_counter() - t0
     slots = n_rows * cfg.L * Dc / cfg.Dn  # channel-fraction-scaled slots of the sample
-    return {"value": slots / dt, "unit": UNIT, "cores": orc.num_threads(), "kind": "oracle",
-            "sample": describe(n_rows, Dc, cfg, dt)}
+    out = {"value": slots / dt, "unit": UNIT, "cores": orc.num_threads(), "kind": "oracle",
+           "sample": describe(n_rows, Dc, cfg, dt)}
+    # the same oracle on ONE host thread, on a 1/cores slice
+    # of the sample's channels so it stays inside the time budget
+    nt = orc.num_threads()
+    if nt > 1:
+        Dc1 = max(16, Dc // nt)
+        s1 = oracle_sample(torch, cfg, n_rows, Dc1, rows_layout)
+        orc.set_num_threads(1)
+        try:
+            t0 = time.perf_counter()
+            oracle_step(orc, cfg, s1)
+            dt1 = time.perf_counter() - t0
+        finally:
+            orc.set_num_threads(nt)
+        out["value_1thread"] = n_rows * cfg.L * Dc1 / cfg.Dn / dt1
+        out["sample_1thread"] = describe(n_rows, Dc1, cfg, dt1)
+    return out
 
 
 def run_reference(args, cfg):
@@ -466,7 +513,7 @@ def main():
     evb = [[torch.cuda.Event(enable_timing=True) for _ in range(nk + 1)] for _ in range(args.steps)]
     torch.cuda.synchronize()
     for i in range(args.steps):
-        step.kernels(evb[i])
+        step.kernels(evb[i], split=True)
     torch.cuda.synchronize()
     if pdl_env is None:
         del os.environ["PM_NO_PDL"]
@@ -487,32 +534,44 @@ def main():
         gbs = ab[n] * slots_rank / t / 1e9
         kern[n] = {"ms": kms[n], "share": kms[n] / ms_local, "hbm_gbs": gbs,
                    "hbm_frac": gbs / peaks["hbm_gbs"]}
-        if n in ALU_OPS:
-            ops = ALU_OPS[n] * slots_rank * cfg.Dn * cfg.N
-            peak_ops = 148 * 128 * peaks["sm_max_mhz"] * 1e6
-            kern[n]["alu_gops"] = ops / t / 1e9
-            kern[n]["alu_frac"] = ops / t / peak_ops
+        if n in FP32_OPS:
+            elems = slots_rank * cfg.Dn * cfg.N
+            kern[n]["fp32_gops"] = FP32_OPS[n] * elems / t / 1e9
+            kern[n]["fp32_frac"] = kern[n]["fp32_gops"] / (peaks["fp32_tops"] * 1e3)
+            kern[n]["mufu_gops"] = MUFU_OPS[n](cfg.N) * elems / t / 1e9
+            kern[n]["mufu_frac"] = kern[n]["mufu_gops"] / (peaks["mufu_tops"] * 1e3)
     if world > 1:
         kern["allreduce"] = {"ms": kms["allreduce"], "share": kms["allreduce"] / ms_local,
                              "bytes": step.pg.nbytes}
     dom = max(names[:4], key=lambda n: kms[n])
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            tr = json.load(f).get(cfg.name, {})
-        traffic = tr.get(dom)
-    if dom in ALU_OPS:
-        roof = {"bound": "alu", "achieved": kern[dom]["alu_gops"],
-                "peak": 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e9, "unit": "Gop/s",
-                "frac": kern[dom]["alu_frac"], "traffic": traffic, "kernel": dom,
-                "peak_source": f"148 SMs x 128 FP32/issue lanes x {peaks['sm_max_mhz']:.0f} MHz "
-                               "(guide unit counts, MEASURED_PEAKS sm_max_mhz)",
-                "hbm_gbs": kern[dom]["hbm_gbs"], "hbm_frac": kern[dom]["hbm_frac"]}
+            tj = json.load(f)
+        traffic = tj.get(cfg.name, {}).get(dom)
+        if traffic is not None:
+            traffic_src = (f"dram__bytes_read.sum + dram__bytes_write.sum per launch from the "
+                           f"committed ncu --set full capture {tj.get('capture', '?')} "
+                           f"(profiles/ncu_traffic.json), not measured in this run")
+    if dom in FP32_OPS:
+        k = kern[dom]
+        # the binding one of the two issue roofs of the scan
+        fp32_bound = k["fp32_frac"] >= k["mufu_frac"]
+        roof = {"bound": "alu", "achieved": k["fp32_gops"] if fp32_bound else k["mufu_gops"],
+                "peak": (peaks["fp32_tops"] if fp32_bound else peaks["mufu_tops"]) * 1e3,
+                "unit": "Gop/s", "frac": max(k["fp32_frac"], k["mufu_frac"]),
+                "pipe": "fp32" if fp32_bound else "mufu",
+                "fp32_frac": k["fp32_frac"], "mufu_frac": k["mufu_frac"],
+                "ops_per_element": {"fp32": FP32_OPS[dom], "mufu": MUFU_OPS[dom](cfg.N)},
+                "elements_per_launch": slots_rank * cfg.Dn * cfg.N,
+                "traffic": traffic, "traffic_source": traffic_src, "kernel": dom,
+                "peak_source": peaks["alu_source"],
+                "hbm_gbs": k["hbm_gbs"], "hbm_frac": k["hbm_frac"]}
     else:
         roof = {"bound": "hbm", "achieved": kern[dom]["hbm_gbs"], "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": kern[dom]["hbm_frac"], "traffic": traffic,
-                "kernel": dom, "peak_source": peaks["source"]}
+                "traffic_source": traffic_src, "kernel": dom, "peak_source": peaks["source"]}
 
     # ---- e2e: same step through the public API with pinned host buffers ----
     e2e = None
@@ -558,10 +617,12 @@ def run_e2e(torch, step, D, dist, world, dev, n, total_slots):
     """End to end through the public API with host buffers, as a pipelined
     data loader would run it: every step copies its inputs host(pinned) ->
     device (x, dt, B, C, dy, pos), runs the 4 kernels (+ all-reduce) and
-    copies dx and the parameter gradients device -> host.  Inputs, dx and the
-    param-grad buffer are double-buffered so step k+1's H2D and step k-1's
-    D2H overlap step k's kernels (copy engines run concurrently with SMs);
-    the timed region spans the first H2D to the last D2H."""
+    copies EVERY output of the path device -> host: y (scan fwd output),
+    ddt, dB, dC, dx and the parameter gradients (du is consumed inside the
+    path by the conv bwd).  Inputs and outputs are double-buffered so step
+    k+1's H2D and step k-1's D2H overlap step k's kernels (copy engines run
+    concurrently with SMs); the timed region spans the first H2D to the last
+    D2H."""
     T, pos = D["T"], D["pos"]
     names = list(T.keys())
     host_in = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in T.items()}
@@ -570,12 +631,14 @@ def run_e2e(torch, step, D, dist, world, dev, n, total_slots):
     host_in["pos"] = torch.empty(pos.shape, dtype=pos.dtype, pin_memory=True)
     host_in["pos"].copy_(pos.cpu())
     dev_in = [{k: torch.empty_like(v, device=dev) for k, v in host_in.items()} for _ in range(2)]
-    dev_dx = [step.dx, torch.empty_like(step.dx)]
-    pgs = [step.pg, D["ParamGrads"](torch, step.cfg.Dn, step.cfg.N, step.cfg.K, dev)]
-    host_dx = [torch.empty(step.dx.shape, dtype=step.dx.dtype, pin_memory=True) for _ in range(2)]
-    host_pg = [torch.empty(step.pg.flat.shape, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+    dev_out = [step.outs(), step.new_outs()]
+    names_out = ["y", "ddt", "dB", "dC", "dx"]
+    host_out = [{k: torch.empty(o[k].shape, dtype=o[k].dtype, pin_memory=True) for k in names_out}
+                for o in dev_out]
+    for b in range(2):
+        host_out[b]["pg"] = torch.empty(step.pg.flat.shape, dtype=torch.float32, pin_memory=True)
     h2d = sum(v.numel() * v.element_size() for v in host_in.values())
-    d2h = host_dx[0].numel() * host_dx[0].element_size() + host_pg[0].numel() * 4
+    d2h = sum(v.numel() * v.element_size() for v in host_out[0].values())
     comp = torch.cuda.current_stream(dev)
     s_in = torch.cuda.Stream(dev)
     s_out = torch.cuda.Stream(dev)
@@ -599,12 +662,13 @@ def run_e2e(torch, step, D, dist, world, dev, n, total_slots):
             comp.wait_event(in_done[b])
             if used[b]:
                 comp.wait_event(out_done[b])
-            step.kernels(inp=dev_in[b], dx=dev_dx[b], pg=pgs[b])
+            step.kernels(inp=dev_in[b], outs=dev_out[b])
             comp_done[b].record(comp)
             with torch.cuda.stream(s_out):
                 s_out.wait_event(comp_done[b])
-                host_dx[b].copy_(dev_dx[b], non_blocking=True)
-                host_pg[b].copy_(pgs[b].flat, non_blocking=True)
+                for k in names_out:
+                    host_out[b][k].copy_(dev_out[b][k], non_blocking=True)
+                host_out[b]["pg"].copy_(dev_out[b]["pg"].flat, non_blocking=True)
                 out_done[b].record(s_out)
             used[b] = True
         comp.wait_event(out_done[(nsteps - 1) % 2])

@@ -205,11 +205,14 @@ PM_API pm_status pm_selective_scan_fwd(const void* u, const void* dt,
  *   The chunk states are only read; the backward claims its work items
  *   through the schedule counters kept in the same buffer (zeroed by the
  *   forward, reset by the backward's last CTA), so one states buffer must
- *   not be used by two backward calls running concurrently.  Enqueued
- *   directly behind its forward kernel the backward is launched
- *   programmatically (PDL): it starts on the SMs the forward's last CTAs
- *   leave and waits per segment until the forward has released that
- *   segment's states (PM_NO_PDL=1 in the environment disables the overlap).
+ *   not be used by two backward calls running concurrently.  This entry
+ *   point launches the backward in plain stream order (it never overlaps
+ *   whatever kernel precedes it); pm_selective_scan_fwd_bwd below runs the
+ *   forward and the backward as one call and overlaps them.  With
+ *   states == NULL the library runs the forward itself right before the
+ *   backward and overlaps the two the same way.  A states buffer whose
+ *   forward did not complete makes the backward trap (sticky CUDA error at
+ *   the next synchronisation) instead of reading unwritten states.
  * workspace: >= pm_selective_scan_bwd_workspace(R, Dn, L, N, states==NULL)
  *   bytes of 16-byte aligned device memory. */
 PM_API size_t pm_selective_scan_bwd_workspace(int64_t R, int64_t Dn, int64_t L,
@@ -290,6 +293,37 @@ PM_API pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt,
                                    size_t ws_bytes, int64_t R, int64_t Dn,
                                    int64_t L, int32_t N, pm_dtype io,
                                    pm_stream_t stream);
+
+/* Forward + backward in one call (activation recompute in training: the
+ * forward is re-run for its chunk states right before the backward):
+ * exactly pm_selective_scan_fwd_ex(u, ..., out, states, h_last, decay)
+ * followed by pm_selective_scan_bwd_ex(u, ..., states, dout, dh_last, ...) on
+ * the same stream, with the same arguments and results.  Because the library
+ * enqueues the backward directly behind its own forward, the backward is
+ * launched programmatically (programmatic dependent launch) when the forward
+ * is throughput-bound: backward CTAs start on the SMs the forward's last CTAs
+ * leave and wait per segment until the forward has released that segment's
+ * states.  Every input of the backward other than the states was written
+ * before the forward started, and the backward's outputs (du, ddt, dA, dB,
+ * dC, dD, ddt_bias, dz, dh0, workspace) must not overlap the forward's
+ * outputs (out, h_last, decay) or any input: overlapping buffers return
+ * PM_ERR_INVALID_ARG.  states is required (pm_selective_scan_state_bytes);
+ * out, h_last, decay may be NULL.  PM_NO_PDL=1 in the environment serializes
+ * the two launches (A/B measurements). */
+PM_API pm_status pm_selective_scan_fwd_bwd(const void* u, const void* dt,
+                                    const float* A, const void* B,
+                                    const void* C, const float* Dskip,
+                                    const float* dt_bias, int32_t dt_softplus,
+                                    int32_t zoh, const int32_t* pos,
+                                    const void* z, const float* h0, void* out,
+                                    float* states, float* h_last, float* decay,
+                                    const void* dout, const float* dh_last,
+                                    void* du, void* ddt, float* dA, float* dB,
+                                    float* dC, float* dD, float* ddt_bias,
+                                    void* dz, float* dh0, void* workspace,
+                                    size_t ws_bytes, int64_t R, int64_t Dn,
+                                    int64_t L, int32_t N, pm_dtype io,
+                                    pm_stream_t stream);
 
 #ifdef __cplusplus
 }

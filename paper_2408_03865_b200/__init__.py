@@ -19,7 +19,7 @@ __all__ = [
     "pm_causal_conv1d_bwd_workspace", "pm_selective_scan_state_bytes",
     "pm_selective_scan_fwd", "pm_selective_scan_bwd",
     "pm_selective_scan_bwd_workspace", "pm_selective_scan_fwd_ex", "pm_selective_scan_bwd_ex",
-    "EXPORTED_SYMBOLS",
+    "pm_selective_scan_fwd_bwd", "EXPORTED_SYMBOLS",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -37,7 +37,7 @@ EXPORTED_SYMBOLS = [
     "pm_pack_planned", "pm_causal_conv1d_fwd", "pm_causal_conv1d_bwd_workspace",
     "pm_causal_conv1d_bwd", "pm_selective_scan_state_bytes", "pm_selective_scan_fwd",
     "pm_selective_scan_bwd_workspace", "pm_selective_scan_bwd", "pm_selective_scan_fwd_ex",
-    "pm_selective_scan_bwd_ex",
+    "pm_selective_scan_bwd_ex", "pm_selective_scan_fwd_bwd",
 ]
 
 
@@ -53,12 +53,16 @@ _lib = None
 
 
 def lib():
-    """Load libpm.so (building it first if the sources are newer)."""
+    """Load libpm.so.  The in-tree library is (re)built first when it is
+    missing or older than its sources (``_build.stale``); a PM_LIB variant is
+    loaded as is."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            from . import _build
-            _build.build()
+        from . import _build
+        if LIB_PATH == _build.LIB:
+            _build.build()  # no-op unless missing or stale
+        elif not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(f"PM_LIB={LIB_PATH} does not exist")
         L = ctypes.CDLL(LIB_PATH)
         L.pm_status_string.restype = ctypes.c_char_p
         L.pm_status_string.argtypes = [ctypes.c_int]
@@ -85,6 +89,8 @@ def lib():
                                                [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
         L.pm_selective_scan_bwd_ex.argtypes = ([_vp] * 7 + [_i32, _i32] + [_vp] * 15 + [_vp, _sz] +
                                                [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
+        L.pm_selective_scan_fwd_bwd.argtypes = ([_vp] * 7 + [_i32, _i32] + [_vp] * 19 + [_sz] +
+                                                [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
         for f in EXPORTED_SYMBOLS:
             if f not in ("pm_status_string", "pm_version") and not f.endswith(
                     ("_workspace", "_bytes")):
@@ -131,6 +137,57 @@ def _dev(*ts):
                 raise RuntimeError("libpm runs on CUDA tensors only (no CPU fallback)")
             if not t.is_contiguous():
                 raise RuntimeError("libpm needs contiguous tensors")
+
+
+def _want(t, name, dtype=None, shape=None):
+    """Argument check before the C call (the C ABI only sees void pointers):
+    dtype and shape of every tensor argument."""
+    if t is None:
+        return
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def _scan_args(u, dt, A, B, C, Dskip, dt_bias, pos, **tok):
+    """Validate the scan's inputs; returns (R, Dn, L, N).  ``tok``: more
+    per-token (R,Dn,L) tensors in the I/O dtype (z, dy, dout, ...)."""
+    import torch
+    if u.dim() != 3:
+        raise ValueError(f"u: expected (R, Dn, L), got shape {tuple(u.shape)}")
+    R, Dn, L = u.shape
+    io = u.dtype
+    _io(u)
+    if A.dim() != 2 or A.shape[0] != Dn:
+        raise ValueError(f"A: expected (Dn={Dn}, N), got shape {tuple(A.shape)}")
+    N = A.shape[1]
+    _want(A, "A", torch.float32)
+    _want(dt, "dt", io, (R, Dn, L))
+    _want(B, "B", io, (R, N, L))
+    _want(C, "C", io, (R, N, L))
+    _want(Dskip, "Dskip", torch.float32, (Dn,))
+    _want(dt_bias, "dt_bias", torch.float32, (Dn,))
+    _want(pos, "pos", torch.int32, (R, L))
+    for k, v in tok.items():
+        _want(v, k, io, (R, Dn, L))
+    return R, Dn, L, N
+
+
+def _conv_args(x, w, bias, pos, **tok):
+    import torch
+    if x.dim() != 3:
+        raise ValueError(f"x: expected (R, Dn, L), got shape {tuple(x.shape)}")
+    R, Dn, L = x.shape
+    _io(x)
+    if w.dim() != 2 or w.shape[0] != Dn:
+        raise ValueError(f"w: expected (Dn={Dn}, K), got shape {tuple(w.shape)}")
+    _want(w, "w", torch.float32)
+    _want(bias, "bias", torch.float32, (Dn,))
+    _want(pos, "pos", torch.int32, (R, L))
+    for k, v in tok.items():
+        _want(v, k, x.dtype, (R, Dn, L))
+    return R, Dn, L, w.shape[1]
 
 
 def _host_i32(a):
@@ -214,7 +271,7 @@ def pm_causal_conv1d_fwd(x, w, bias, pos, out=None, silu=True):
     """Alg 1 conv1d_pack forward: x (R,Dn,L) f32|bf16, w (Dn,K) f32, pos (R,L) i32."""
     import torch
     _dev(x, w, bias, pos)
-    R, Dn, L = x.shape
+    R, Dn, L, _ = _conv_args(x, w, bias, pos, out=out)
     out = torch.empty_like(x) if out is None else out
     _dev(out)
     _check(lib().pm_causal_conv1d_fwd(_ptr(x), _ptr(w), _ptr(bias), _ptr(pos), _ptr(out), R, Dn,
@@ -232,8 +289,9 @@ def pm_causal_conv1d_bwd(x, w, bias, pos, dout, dx=None, dw=None, dbias=None, si
     """Adjoint of conv1d_pack -> (dx, dw, dbias)."""
     import torch
     _dev(x, w, bias, pos, dout)
-    R, Dn, L = x.shape
-    K = w.shape[1]
+    R, Dn, L, K = _conv_args(x, w, bias, pos, dout=dout, dx=dx)
+    _want(dw, "dw", torch.float32, (Dn, K))
+    _want(dbias, "dbias", torch.float32, (Dn,))
     dx = torch.empty_like(x) if dx is None else dx
     dw = torch.empty_like(w) if dw is None else dw
     if dbias is None and bias is not None:
@@ -253,6 +311,27 @@ def pm_causal_conv1d_bwd(x, w, bias, pos, dout, dx=None, dw=None, dbias=None, si
 # ScanOp_pack
 # ----------------------------------------------------------------------------
 
+def _states_ok(states, R, Dn, L, N):
+    import torch
+    if states is None:
+        return
+    _want(states, "states", torch.float32)
+    if states.numel() * 4 < pm_selective_scan_state_bytes(R, Dn, L, N):
+        raise ValueError("states: smaller than pm_selective_scan_state_bytes()")
+
+
+def _grad_outs(o, R, Dn, L, N, io):
+    """Check caller-supplied gradient outputs (dtype and shape)."""
+    import torch
+    f32 = torch.float32
+    spec = dict(du=(io, (R, Dn, L)), ddt=(io, (R, Dn, L)), dz=(io, (R, Dn, L)),
+                dA=(f32, (Dn, N)), dB=(f32, (R, N, L)), dC=(f32, (R, N, L)), dD=(f32, (Dn,)),
+                ddt_bias=(f32, (Dn,)), dh0=(f32, (R, Dn, N)))
+    for k, v in o.items():
+        if k in spec:
+            _want(v, k, *spec[k])
+
+
 def pm_selective_scan_state_bytes(R, Dn, L, N):
     return int(lib().pm_selective_scan_state_bytes(R, Dn, L, N))
 
@@ -266,8 +345,7 @@ def pm_selective_scan_fwd(u, dt, A, B, C, Dskip, dt_bias, pos, y=None, states=No
     """ScanOp_pack forward (Alg 2; Eq 1a/1b/2a).  Returns (y, states)."""
     import torch
     _dev(u, dt, A, B, C, Dskip, dt_bias, pos)
-    R, Dn, L = u.shape
-    N = A.shape[1]
+    R, Dn, L, N = _scan_args(u, dt, A, B, C, Dskip, dt_bias, pos, y=y)
     y = torch.empty_like(u) if y is None else y
     if states is None and want_states:
         nb = pm_selective_scan_state_bytes(R, Dn, L, N)
@@ -287,9 +365,10 @@ def pm_selective_scan_bwd(u, dt, A, B, C, Dskip, dt_bias, pos, dy, states=None,
     ``out`` may supply preallocated outputs (same keys)."""
     import torch
     _dev(u, dt, A, B, C, Dskip, dt_bias, pos, dy, states)
-    R, Dn, L = u.shape
-    N = A.shape[1]
+    R, Dn, L, N = _scan_args(u, dt, A, B, C, Dskip, dt_bias, pos, dy=dy)
+    _states_ok(states, R, Dn, L, N)
     o = dict(out or {})
+    _grad_outs(o, R, Dn, L, N, u.dtype)
     dev = u.device
     f32 = dict(dtype=torch.float32, device=dev)
     o.setdefault("du", torch.empty_like(u))
@@ -323,8 +402,9 @@ def pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, z=None, h0=Non
     decay when want_decay."""
     import torch
     _dev(u, dt, A, B, C, Dskip, dt_bias, pos, z, h0)
-    R, Dn, L = u.shape
-    N = A.shape[1]
+    R, Dn, L, N = _scan_args(u, dt, A, B, C, Dskip, dt_bias, pos, z=z, out=out)
+    for k, v in (("h0", h0), ("h_last", h_last), ("decay", decay)):
+        _want(v, k, torch.float32, (R, Dn, N))
     out = torch.empty_like(u) if out is None else out
     if states is None and want_states:
         nb = pm_selective_scan_state_bytes(R, Dn, L, N)
@@ -351,9 +431,12 @@ def pm_selective_scan_bwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, dout, z=None, 
     dD, ddt_bias, dz (when z is given), dh0 (when h0 is given or want_dh0)."""
     import torch
     _dev(u, dt, A, B, C, Dskip, dt_bias, pos, dout, z, h0, states, dh_last)
-    R, Dn, L = u.shape
-    N = A.shape[1]
+    R, Dn, L, N = _scan_args(u, dt, A, B, C, Dskip, dt_bias, pos, dout=dout, z=z)
+    for k, v in (("h0", h0), ("dh_last", dh_last)):
+        _want(v, k, torch.float32, (R, Dn, N))
+    _states_ok(states, R, Dn, L, N)
     o = dict(out or {})
+    _grad_outs(o, R, Dn, L, N, u.dtype)
     dev = u.device
     f32 = dict(dtype=torch.float32, device=dev)
     o.setdefault("du", torch.empty_like(u))
@@ -380,3 +463,49 @@ def pm_selective_scan_bwd_ex(u, dt, A, B, C, Dskip, dt_bias, pos, dout, z=None, 
         _ptr(workspace), workspace.numel(), R, Dn, L, N, _io(u), _stream(u)),
         "pm_selective_scan_bwd_ex")
     return o
+
+
+def pm_selective_scan_fwd_bwd(u, dt, A, B, C, Dskip, dt_bias, pos, dout, states, z=None,
+                              h0=None, out=None, h_last=None, decay=None, dh_last=None,
+                              dt_softplus=True, zoh=False, grads=None, workspace=None,
+                              want_dh0=None):
+    """Forward + backward in one call (pm.h: the backward launched
+    programmatically behind the library's own forward).  ``states`` is
+    required (pm_selective_scan_state_bytes); ``out``/``h_last``/``decay``
+    are optional forward outputs.  Returns (out, grads) with grads the dict
+    of pm_selective_scan_bwd_ex."""
+    import torch
+    _dev(u, dt, A, B, C, Dskip, dt_bias, pos, dout, z, h0, states, dh_last, out, h_last, decay)
+    R, Dn, L, N = _scan_args(u, dt, A, B, C, Dskip, dt_bias, pos, dout=dout, z=z, out=out)
+    for k, v in (("h0", h0), ("dh_last", dh_last), ("h_last", h_last), ("decay", decay)):
+        _want(v, k, torch.float32, (R, Dn, N))
+    if states is None:
+        raise ValueError("states is required")
+    _states_ok(states, R, Dn, L, N)
+    o = dict(grads or {})
+    _grad_outs(o, R, Dn, L, N, u.dtype)
+    dev = u.device
+    f32 = dict(dtype=torch.float32, device=dev)
+    o.setdefault("du", torch.empty_like(u))
+    o.setdefault("ddt", torch.empty_like(u))
+    o.setdefault("dA", torch.empty((Dn, N), **f32))
+    o.setdefault("dB", torch.empty((R, N, L), **f32))
+    o.setdefault("dC", torch.empty((R, N, L), **f32))
+    o.setdefault("dD", torch.empty((Dn,), **f32) if Dskip is not None else None)
+    o.setdefault("ddt_bias", torch.empty((Dn,), **f32) if dt_bias is not None else None)
+    o.setdefault("dz", torch.empty_like(u) if z is not None else None)
+    if want_dh0 is None:
+        want_dh0 = h0 is not None
+    o.setdefault("dh0", torch.empty((R, Dn, N), **f32) if want_dh0 else None)
+    need = pm_selective_scan_bwd_workspace(R, Dn, L, N, False)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    _dev(workspace, *[v for v in o.values() if v is not None])
+    _check(lib().pm_selective_scan_fwd_bwd(
+        _ptr(u), _ptr(dt), _ptr(A), _ptr(B), _ptr(C), _ptr(Dskip), _ptr(dt_bias),
+        int(bool(dt_softplus)), int(bool(zoh)), _ptr(pos), _ptr(z), _ptr(h0), _ptr(out),
+        _ptr(states), _ptr(h_last), _ptr(decay), _ptr(dout), _ptr(dh_last), _ptr(o["du"]),
+        _ptr(o["ddt"]), _ptr(o["dA"]), _ptr(o["dB"]), _ptr(o["dC"]), _ptr(o["dD"]),
+        _ptr(o["ddt_bias"]), _ptr(o["dz"]), _ptr(o["dh0"]), _ptr(workspace), workspace.numel(),
+        R, Dn, L, N, _io(u), _stream(u)), "pm_selective_scan_fwd_bwd")
+    return out, o

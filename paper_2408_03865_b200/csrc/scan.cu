@@ -133,16 +133,19 @@ pm_status pm_selective_scan_fwd(const void* u, const void* dt, const float* A, c
                                   nullptr, y, states, nullptr, nullptr, R, Dn, L, N, io, stream);
 }
 
-pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A, const void* B,
-                                   const void* C, const float* Dskip, const float* dt_bias,
-                                   int32_t dt_softplus, int32_t zoh, const int32_t* pos,
-                                   const void* z,
-                                   const float* h0, float* states, const void* dout,
-                                   const float* dh_last, void* du, void* ddt, float* dA,
-                                   float* dB, float* dC, float* dD, float* ddt_bias, void* dz,
-                                   float* dh0, void* workspace, size_t ws_bytes, int64_t R,
-                                   int64_t Dn, int64_t L, int32_t N, pm_dtype io,
-                                   pm_stream_t stream) {
+}  // extern "C"
+
+namespace {
+// The backward.  pdl: the caller (this library) has enqueued the forward that
+// fills `states` directly before this call on the same stream, so the
+// backward may launch programmatically behind it (pm.h).
+pm_status bwd_impl(const void* u, const void* dt, const float* A, const void* B, const void* C,
+                   const float* Dskip, const float* dt_bias, int32_t dt_softplus, int32_t zoh,
+                   const int32_t* pos, const void* z, const float* h0, float* states,
+                   const void* dout, const float* dh_last, void* du, void* ddt, float* dA,
+                   float* dB, float* dC, float* dD, float* ddt_bias, void* dz, float* dh0,
+                   void* workspace, size_t ws_bytes, int64_t R, int64_t Dn, int64_t L, int32_t N,
+                   pm_dtype io, pm_stream_t stream, bool pdl) {
   pm_status st = check_common(R, Dn, L, N, io);
   if (st != PM_OK) return st;
   if (!u || !dt || !A || !B || !C || !pos || !dout || !du || !ddt || !dA || !dB || !dC ||
@@ -161,7 +164,7 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
   const int isz = io == PM_F32 ? 4 : 2;
   const bool vec = (L * isz) % 16 == 0 && Dn % 4 == 0 && aligned16(u) && aligned16(dt) &&
                    aligned16(B) && aligned16(C) && aligned16(dout) && aligned16(du) &&
-                   aligned16(ddt) && aligned16(z) && aligned16(dz);
+                   aligned16(ddt) && aligned16(z) && aligned16(dz) && aligned16(pos);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   char* w = static_cast<char*>(workspace);
   float* ws_bc = reinterpret_cast<float*>(w);
@@ -186,6 +189,7 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
     pm_status fs = run_scan_fwd(fa, (int)N, fvec, io, s);
     if (fs != PM_OK) return fs;
     stp = st_ws;
+    pdl = true;  // the library's own forward is the preceding launch
   }
   // the length-sorted segment list, work counters and per-segment done
   // counts written by the forward pass (in the states buffer)
@@ -195,12 +199,95 @@ pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A
                 sc.sorted, sc.counters + 1, sc.done, (int)(R * n_seg(L)),
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
                 z, h0, dh_last, dz, dh0, zoh ? 1 : 0};
+  a.pdl = pdl ? 1 : 0;
   // TMA for the per-chunk inputs when the vector path applies (row strides
   // are then multiples of 16 bytes); cp.async otherwise.  PM_NO_TMA=1 forces
   // cp.async (A/B measurements).
   a.use_tma = vec && Dn % 4 == 0 && getenv("PM_NO_TMA") == nullptr &&
               encode_bwd_maps(a, (int)N, io) ? 1 : 0;
   return run_scan_bwd(a, (int)N, vec, io, dA, dB, dC, dD, ddt_bias, s);
+}
+
+struct Span {
+  const void* p;
+  size_t n;
+};
+bool overlap(Span a, Span b) {
+  if (a.p == nullptr || b.p == nullptr || a.n == 0 || b.n == 0) return false;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(a.p), b0 = reinterpret_cast<uintptr_t>(b.p);
+  return a0 < b0 + b.n && b0 < a0 + a.n;
+}
+}  // namespace
+
+extern "C" {
+
+pm_status pm_selective_scan_bwd_ex(const void* u, const void* dt, const float* A, const void* B,
+                                   const void* C, const float* Dskip, const float* dt_bias,
+                                   int32_t dt_softplus, int32_t zoh, const int32_t* pos,
+                                   const void* z,
+                                   const float* h0, float* states, const void* dout,
+                                   const float* dh_last, void* du, void* ddt, float* dA,
+                                   float* dB, float* dC, float* dD, float* ddt_bias, void* dz,
+                                   float* dh0, void* workspace, size_t ws_bytes, int64_t R,
+                                   int64_t Dn, int64_t L, int32_t N, pm_dtype io,
+                                   pm_stream_t stream) {
+  return bwd_impl(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, zoh, pos, z, h0, states, dout,
+                  dh_last, du, ddt, dA, dB, dC, dD, ddt_bias, dz, dh0, workspace, ws_bytes, R, Dn,
+                  L, N, io, stream, false);
+}
+
+pm_status pm_selective_scan_fwd_bwd(const void* u, const void* dt, const float* A, const void* B,
+                                    const void* C, const float* Dskip, const float* dt_bias,
+                                    int32_t dt_softplus, int32_t zoh, const int32_t* pos,
+                                    const void* z, const float* h0, void* out, float* states,
+                                    float* h_last, float* decay, const void* dout,
+                                    const float* dh_last, void* du, void* ddt, float* dA,
+                                    float* dB, float* dC, float* dD, float* ddt_bias, void* dz,
+                                    float* dh0, void* workspace, size_t ws_bytes, int64_t R,
+                                    int64_t Dn, int64_t L, int32_t N, pm_dtype io,
+                                    pm_stream_t stream) {
+  pm_status st = check_common(R, Dn, L, N, io);
+  if (st != PM_OK) return st;
+  if (states == nullptr) return PM_ERR_INVALID_ARG;
+  // The backward may start before the forward has finished: none of its
+  // outputs may overlap a forward output or an input, and no forward output
+  // may be an input of the backward.
+  const size_t isz = io == PM_F32 ? 4 : 2;
+  const size_t tok = (size_t)R * Dn * L * isz, bc = (size_t)R * N * L, rdn = (size_t)R * Dn * N * 4;
+  const Span fwd_out[] = {{out, tok}, {h_last, rdn}, {decay, rdn},
+                          {states, state_bytes(R, Dn, L, N)}};
+  const Span bwd_out[] = {{du, tok}, {ddt, tok}, {dA, (size_t)Dn * N * 4}, {dB, bc * 4},
+                          {dC, bc * 4}, {dD, (size_t)Dn * 4}, {ddt_bias, (size_t)Dn * 4},
+                          {dz, tok}, {dh0, rdn}, {workspace, ws_bytes}};
+  const Span inputs[] = {{u, tok}, {dt, tok}, {A, (size_t)Dn * N * 4}, {B, bc * isz},
+                         {C, bc * isz}, {Dskip, (size_t)Dn * 4}, {dt_bias, (size_t)Dn * 4},
+                         {pos, (size_t)R * L * 4}, {z, tok}, {h0, rdn}, {dout, tok},
+                         {dh_last, rdn}};
+  for (const Span& o : bwd_out) {
+    for (const Span& f : fwd_out)
+      if (overlap(o, f)) return PM_ERR_INVALID_ARG;
+    for (const Span& i : inputs)
+      if (overlap(o, i)) return PM_ERR_INVALID_ARG;
+  }
+  for (const Span& f : fwd_out)
+    for (const Span& i : inputs)
+      if (overlap(f, i)) return PM_ERR_INVALID_ARG;
+  // validate the backward's arguments before the forward is enqueued
+  if (!dout || !du || !ddt || !dA || !dB || !dC || (z != nullptr) != (dz != nullptr))
+    return PM_ERR_INVALID_ARG;
+  if (!workspace || ws_bytes < bwd_ws_bytes(R, Dn, L, N, false)) return PM_ERR_WORKSPACE;
+  if (!aligned16(workspace)) return PM_ERR_ALIGN;
+  for (const void* p : {dout, (const void*)du, (const void*)ddt, (const void*)dz})
+    if (!elem_aligned(p, io)) return PM_ERR_ALIGN;
+  for (const void* p : {(const void*)dA, (const void*)dB, (const void*)dC, (const void*)dD,
+                        (const void*)ddt_bias, (const void*)dh_last, (const void*)dh0})
+    if (p && (reinterpret_cast<uintptr_t>(p) & 3u)) return PM_ERR_ALIGN;
+  st = pm_selective_scan_fwd_ex(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, zoh, pos, z, h0, out,
+                                states, h_last, decay, R, Dn, L, N, io, stream);
+  if (st != PM_OK) return st;
+  return bwd_impl(u, dt, A, B, C, Dskip, dt_bias, dt_softplus, zoh, pos, z, h0, states, dout,
+                  dh_last, du, ddt, dA, dB, dC, dD, ddt_bias, dz, dh0, workspace, ws_bytes, R, Dn,
+                  L, N, io, stream, true);
 }
 
 pm_status pm_selective_scan_bwd(const void* u, const void* dt, const float* A, const void* B,

@@ -10,7 +10,21 @@
 #define PM_BWD_UNROLL 4
 #endif
 
+#ifndef PM_BWD_LANEFIN  // each lane of a pair finishes one step of a round (else both, every step)
+#define PM_BWD_LANEFIN 1
+#endif
+#ifndef PM_BWD_SCSWZ  // XOR-swizzled columns of the per-(t,d) scalar rows (bank conflicts)
+#define PM_BWD_SCSWZ 1
+#endif
+
 namespace pm {
+
+// Column of channel c in row ii of the scalar buffer sc[kChunk][kBwdCh]: the
+// rows written together (phase 1: ii and ii + 8 by a lane pair; the park of a
+// round: ii and ii + 1) land in opposite 16-bank halves.
+PM_DEV int sc_col(int ii, int c) {
+  return PM_BWD_SCSWZ ? c ^ ((((ii >> 3) ^ ii) & 1) << 2) : c;
+}
 
 constexpr int kBwdUnroll = PM_BWD_UNROLL;
 constexpr int kBwdAUnroll = PM_BWD_AUNROLL;
@@ -40,18 +54,6 @@ constexpr int kBwdAUnroll = PM_BWD_AUNROLL;
 //            chunk's du/ddt rows leave with full-sector vector stores.
 
 template <typename T, int N, bool kGate>
-struct BwdRaw {  // raw inputs of one chunk, filled by TMA or cp.async (vector path)
-  alignas(128) T u[kBwdCh][kChunk];
-  alignas(128) T dt[kBwdCh][kChunk];
-  alignas(128) T dy[kBwdCh][kChunk];
-  alignas(128) T B[N][kChunk];
-  alignas(128) T C[N][kChunk];
-  alignas(128) int32_t pos[kChunk];
-  alignas(128) float st[N][kBwdCh];
-  alignas(128) T z[kGate ? kBwdCh : 1][kChunk];
-};
-
-template <typename T, int N, bool kGate>
 struct BwdSmem {
   static constexpr int NH = N / 2;   // states per thread
   static constexpr int kQ = N / 4;   // float4 quads of (dB, dC) values per thread-step
@@ -73,73 +75,6 @@ struct BwdSmem {
   int s_red[kBwdWarps];
   uint32_t tmem_base;
 };
-
-// Issue the cp.async copies of chunk c's raw inputs (vector path only:
-// L*isz % 16 == 0, Dn % 4 == 0, 16-byte aligned pointers).
-template <typename T, int N, bool kGate>
-PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, int dblk, int c,
-                          int s0, uint64_t* bar) {
-  constexpr int kEl = 16 / (int)sizeof(T);       // elements per 16-byte chunk
-  constexpr int kRowQ = kChunk / kEl;            // chunks per (row, chunk)
-  const int L = a.L, Dn = a.Dn, cb = c * kChunk;
-  const bool with_st = cb > s0 || (cb == 0 && a.h0 != nullptr);
-  if (a.use_tma) {  // one thread issues the chunk's bulk tensor copies
-    if (threadIdx.x == 0) {
-      constexpr uint32_t kRows = kBwdCh * kChunk * sizeof(T);
-      const uint32_t bytes = (kGate ? 4 : 3) * kRows + 2 * N * kChunk * sizeof(T) +
-                             kChunk * sizeof(int32_t) + (with_st ? N * kBwdCh * sizeof(float) : 0);
-      mbar_expect_tx(bar, bytes);
-      const int d0 = dblk * kBwdCh;
-      tma_load<3>(rw.u, &a.tm_u, bar, cb, d0, r);
-      tma_load<3>(rw.dt, &a.tm_dt, bar, cb, d0, r);
-      tma_load<3>(rw.dy, &a.tm_dy, bar, cb, d0, r);
-      if constexpr (kGate) tma_load<3>(rw.z, &a.tm_z, bar, cb, d0, r);
-      tma_load<3>(rw.B, &a.tm_B, bar, cb, 0, r);
-      tma_load<3>(rw.C, &a.tm_C, bar, cb, 0, r);
-      tma_load<2>(rw.pos, &a.tm_pos, bar, cb, r);
-      if (with_st) tma_load<4>(rw.st, &a.tm_st, bar, d0, 0, c, r);
-    }
-    return;
-  }
-  constexpr int kTx = kBwdCh * kRowQ;
-#pragma unroll
-  for (int arr = 0; arr < (kGate ? 4 : 3); ++arr) {  // u, dt, dy (, z)
-    const T* base = static_cast<const T*>(arr == 0 ? a.u : arr == 1 ? a.dt : arr == 2 ? a.dy : a.z);
-    T(*dst)[kChunk] = arr == 0 ? rw.u : arr == 1 ? rw.dt : arr == 2 ? rw.dy : rw.z;
-    for (int e = threadIdx.x; e < kTx; e += kBwdThreads) {
-      const int ch = e / kRowQ, q = e % kRowQ;
-      const int d = dblk * kBwdCh + ch;
-      const int t0 = cb + q * kEl;
-      const bool ok = d < Dn && t0 < L;
-      const T* src = ok ? base + ((int64_t)r * Dn + d) * L + t0 : base;
-      cp_async16(&dst[ch][q * kEl], src, ok ? 16 : 0);
-    }
-  }
-  const T* Bp = static_cast<const T*>(a.B) + (int64_t)r * N * L;
-  const T* Cp = static_cast<const T*>(a.C) + (int64_t)r * N * L;
-  for (int e = threadIdx.x; e < 2 * N * kRowQ; e += kBwdThreads) {
-    const int arr = e / (N * kRowQ), rem = e % (N * kRowQ), n = rem / kRowQ, q = rem % kRowQ;
-    const int t0 = cb + q * kEl;
-    const bool ok = t0 < L;
-    const T* src = (arr == 0 ? Bp : Cp) + (int64_t)n * L + (ok ? t0 : 0);
-    cp_async16(&(arr == 0 ? rw.B : rw.C)[n][q * kEl], src, ok ? 16 : 0);
-  }
-  for (int e = threadIdx.x; e < kChunk / 4; e += kBwdThreads) {
-    const int t0 = cb + 4 * e;
-    const bool ok = t0 < L;
-    cp_async16(&rw.pos[4 * e], a.pos + (int64_t)r * L + (ok ? t0 : 0), ok ? 16 : 0);
-  }
-  if (with_st) {
-    for (int e = threadIdx.x; e < N * (kBwdCh / 4); e += kBwdThreads) {
-      const int n = e / (kBwdCh / 4), q = e % (kBwdCh / 4);
-      const int d0 = dblk * kBwdCh + 4 * q;
-      const bool ok = d0 < Dn;
-      const float* src = a.states + (((int64_t)r * a.nchunk + c) * N + n) * Dn + (ok ? d0 : 0);
-      cp_async16(&rw.st[n][4 * q], src, ok ? 16 : 0);
-    }
-  }
-  cp_async_commit();
-}
 
 template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh>
 __global__ void __launch_bounds__(kBwdThreads, MinB)
@@ -176,12 +111,18 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
       if (w < a.n_items * ndblk && a.done != nullptr) {
         // this kernel may run while the forward's last items are still in
         // flight (programmatic launch): wait until every forward channel
-        // block of this segment has released its states (bounded: a states
-        // buffer not written by the forward must not hang the GPU)
+        // block of this segment has released its states
         const int4 it = a.items[w / ndblk];
         const int* dp = a.done + it.x * a.nseg + it.y;
         const int need = a.Dn;  // every channel of the segment released by the forward
-        for (int spin = 0; spin < (1 << 22) && ld_acquire(dp) < need; ++spin) __nanosleep(256);
+        // (bounded: a states buffer its forward never completed must not
+        // hang the GPU; after ~1-4 s the kernel traps -- a sticky error at the
+        // caller's next synchronisation -- instead of reading unwritten states)
+        int spin = 0;
+        while (ld_acquire(dp) < need) {
+          if (++spin > (1 << 24)) __trap();
+          __nanosleep(256);
+        }
         fence_proxy_async_global();  // the states are read by TMA (async proxy)
       }
     }
@@ -311,7 +252,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
           dyv = yy[i] * zz[i] * sz;
           sm.sgz[ii][cl] = active ? yy[i] * sz * fmaf(zz[i], 1.f - sz, 1.f) : 0.f;
         }
-        sm.sc[ii][cl] = make_float4(dl, active ? uu[i] : 0.f, active ? dyv : 0.f, sg);
+        sm.sc[ii][sc_col(ii, cl)] = make_float4(dl, active ? uu[i] : 0.f, active ? dyv : 0.f, sg);
       }
       if constexpr (kVec) {
         // transpose [n][t] -> [t][n], two steps per thread (contiguous reads)
@@ -365,7 +306,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
       const int t = cb + ii;
       tmem_st<NH>(tbase + (uint32_t)(ii * NH), reinterpret_cast<const float*>(h));
       if (!kFull && (t < c0 || t >= c1)) return;  // CTA-uniform
-      const float4 scv = sm.sc[ii][cl];
+      const float4 scv = sm.sc[ii][sc_col(ii, cl)];
       const float2 dl2 = f2(scv.x), dux2 = f2(scv.x * scv.y);
       const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
       if constexpr (kZoh) {  // B-bar u = f(z) delta B u (Eq 2b)
@@ -412,7 +353,11 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
         for (int p = 0; p < NP; ++p) h[p] = hp[0][p];
         return;
       }
+      constexpr bool kLaneFin = PM_BWD_LANEFIN && !kZoh && kBSub == 2;
       float duo[kBSub], ddo[kBSub], dzo[kBSub];
+      float Sv[kBSub], dqv[kBSub], yvv[kBSub];  // this lane's partial sums (kLaneFin)
+      float fdu = 0.f, fddt = 0.f, fdz = 0.f;   // (du, ddt, dz) of step a0 + hf (kLaneFin)
+      float4 sci[kBSub];                        // the steps' scalars (kLaneFin)
 #pragma unroll
       for (int i = kBSub - 1; i >= 0; --i) {
         const int t = a0 + i, ii = t - cb;
@@ -425,9 +370,11 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
           duo[i] = 0.f;
           ddo[i] = 0.f;
           dzo[i] = 0.f;
+          Sv[i] = dqv[i] = yvv[i] = 0.f;
+          sci[i] = make_float4(0.f, 0.f, 0.f, 0.f);
           continue;
         }
-        const float4 scv = sm.sc[ii][cl];
+        const float4 scv = sm.sc[ii][sc_col(ii, cl)];
         const float delta = scv.x, ux = scv.y, dyv = scv.z;
         const float2 dl2 = f2(delta), dux2 = f2(delta * ux), dy2 = f2(dyv);
         const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
@@ -489,6 +436,21 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
           }
         }
         float Ssum = Sp.x + Sp.y, dq = dqp.x + dqp.y;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+          rslot(q) = make_float4(vals[2 * q].x, vals[2 * q].y, vals[2 * q + 1].x, vals[2 * q + 1].y);
+        if constexpr (kLaneFin) {  // finished after the round by one lane per step
+          Sv[i] = Ssum;
+          dqv[i] = dq;
+          sci[i] = scv;
+          if constexpr (kGate) {
+            float2 yp = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) yp = ffma2(Ct[p], hc[p], yp);
+            yvv[i] = yp.x + yp.y;
+          }
+          continue;
+        }
         if constexpr (kGate) {  // y_t = C_t . h_t + D u_t (pre-gate) for dz
           float2 yp = make_float2(0.f, 0.f);
 #pragma unroll
@@ -497,9 +459,6 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
           yv += __shfl_xor_sync(0xffffffffu, yv, 1);
           dzo[i] = fmaf(Dd, ux, yv) * sm.sgz[ii][cl];
         }
-#pragma unroll
-        for (int q = 0; q < kQ; ++q)
-          rslot(q) = make_float4(vals[2 * q].x, vals[2 * q].y, vals[2 * q + 1].x, vals[2 * q + 1].y);
         Ssum += __shfl_xor_sync(0xffffffffu, Ssum, 1);
         dq += __shfl_xor_sync(0xffffffffu, dq, 1);
         if constexpr (kZoh) {  // Ssum already carries bfac (which includes delta)
@@ -513,6 +472,26 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
         }
         dD = fmaf(dyv, ux, dD);
         ddtb += ddo[i];
+      }
+      if constexpr (kLaneFin) {
+        // lane hf finishes step a0 + hf: the pair's sums of that step (one
+        // shuffle per value: send the partner's step, keep mine)
+        auto pair_sum = [&](const float (&v)[kBSub]) {
+          const float keep = hf ? v[1] : v[0], send = hf ? v[0] : v[1];
+          return keep + __shfl_xor_sync(0xffffffffu, send, 1);
+        };
+        const float S = pair_sum(Sv), dq = pair_sum(dqv);
+        float yt = 0.f;
+        if constexpr (kGate) yt = pair_sum(yvv);
+        const float4 scv = hf ? sci[1] : sci[0];
+        const int t = a0 + hf;
+        if (kFull || (t >= c0 && t < c1)) {
+          fdu = fmaf(Dd, scv.z, scv.x * S);
+          fddt = fmaf(scv.y, S, dq * kLn2) * scv.w;
+          if constexpr (kGate) fdz = fmaf(Dd, scv.y, yt) * sm.sgz[t - cb][cl];
+          dD = fmaf(scv.z, scv.y, dD);
+          ddtb += fddt;
+        }
       }
 #pragma unroll
       for (int p = 0; p < NP; ++p) h[p] = hp[0][p];
@@ -545,10 +524,15 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
       __syncwarp();
       // the step's scalars are consumed: park (du, ddt, dz) in their slot;
       // the chunk's rows are written to HBM with full-sector stores below
-      if (hf == 0) {
+      if constexpr (kLaneFin) {
+        const int ii = a0 - cb + hf;
+        sm.sc[ii][sc_col(ii, cl)] = make_float4(fdu, fddt, fdz, 0.f);
+      } else if (hf == 0) {
 #pragma unroll
-        for (int i = 0; i < kBSub; ++i)
-          sm.sc[a0 - cb + i][cl] = make_float4(duo[i], ddo[i], dzo[i], 0.f);
+        for (int i = 0; i < kBSub; ++i) {
+          const int ii = a0 - cb + i;
+          sm.sc[ii][sc_col(ii, cl)] = make_float4(duo[i], ddo[i], dzo[i], 0.f);
+        }
       }
     };
     if constexpr (kFull) {
@@ -620,13 +604,17 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
         float v[2][8];
 #pragma unroll
         for (int ii = 0; ii < kChunk; ++ii) {
-          const float4 q = sm.sc[ii][cc];
+          const float4 q = sm.sc[ii][sc_col(ii, cc)];
           v[ii >> 3][ii & 7] = which == 0 ? q.x : which == 1 ? q.y : q.z;
         }
         store8<T, kVec>(dst, cb, c0, c1, v[0]);
         store8<T, kVec>(dst, cb + 8, c0, c1, v[1]);
       }
     }
+  }
+  if (PM_BWD_LANEFIN && !kZoh) {  // each lane of the pair summed its own steps
+    dD += __shfl_xor_sync(0xffffffffu, dD, 1);
+    ddtb += __shfl_xor_sync(0xffffffffu, ddtb, 1);
   }
   if (active) {
 #pragma unroll
@@ -779,13 +767,30 @@ pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
     // segments are the forward's critical path (mean load << L, e.g. the
     // 130m config: 332 of 2048 steps) backward CTAs sharing those SMs slow
     // that path down (measured +11 % step), so the launch stays serialized.
-    const bool pdl = a.done != nullptr && getenv("PM_NO_PDL") == nullptr &&
+    // Only when the library itself enqueued the forward right before this
+    // launch (pm_selective_scan_fwd_bwd, recompute path): a programmatic
+    // launch waits on nothing but the states, so any other predecessor's
+    // outputs would be unordered (pm.h).
+    const bool pdl = a.pdl && a.done != nullptr && getenv("PM_NO_PDL") == nullptr &&
                      (getenv("PM_PDL") != nullptr || fwd_throughput_bound(a.R, a.L, a.Dn));
     cfg.numAttrs = pdl ? 1 : 0;
     if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return PM_ERR_CUDA;
   } else {
     kern<<<dim3(n_dblk_bwd(a.Dn), a.R, a.nseg), kBwdThreads, smem, s>>>(a);
   }
+  PM_LAUNCH_CHECK();
+  return PM_OK;
+}
+
+template <int N>
+pm_status finalize_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, float* dD,
+                       float* ddtb, cudaStream_t s) {
+  dim3 g2((a.L + 31) / 32, a.R);
+  scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
+  PM_LAUNCH_CHECK();
+  const int64_t np = (int64_t)(N + 2) * a.Dn;
+  scan_bwd_finalize_param<N><<<(unsigned)((np + 31) / 32), 256, 0, s>>>(
+      a.ws_param, dA, dD, ddtb, a.R * a.nseg, a.Dn);
   PM_LAUNCH_CHECK();
   return PM_OK;
 }
@@ -799,14 +804,7 @@ pm_status launch_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, floa
             : (a.z != nullptr ? launch_bwd_k<T, N, kVec, true, false>(a, s)
                               : launch_bwd_k<T, N, kVec, false, false>(a, s));
   if (st != PM_OK) return st;
-  dim3 g2((a.L + 31) / 32, a.R);
-  scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
-  PM_LAUNCH_CHECK();
-  const int64_t np = (int64_t)(N + 2) * a.Dn;
-  scan_bwd_finalize_param<N><<<(unsigned)((np + 31) / 32), 256, 0, s>>>(
-      a.ws_param, dA, dD, ddtb, a.R * a.nseg, a.Dn);
-  PM_LAUNCH_CHECK();
-  return PM_OK;
+  return finalize_bwd<N>(a, dA, dB, dC, dD, ddtb, s);
 }
 
 template <typename T, int N>

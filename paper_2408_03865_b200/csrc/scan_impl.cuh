@@ -109,6 +109,7 @@ struct ScanBwdArgs {
   // back to cp.async): (L, Dn, R) u/dt/dy/z, (L, N, R) B/C, (L, R) pos,
   // (Dn, N, nchunk, R) states
   int use_tma;
+  int pdl;  // launched programmatically behind the library's own forward (pm.h)
   CUtensorMap tm_u, tm_dt, tm_dy, tm_z, tm_B, tm_C, tm_pos, tm_st;
 };
 
@@ -144,6 +145,87 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Raw inputs of one backward chunk of kBwdCh channels (shared by the backward kernel and its staging helper)
+template <typename T, int N, bool kGate>
+struct BwdRaw {  // raw inputs of one chunk, filled by TMA or cp.async (vector path)
+  alignas(128) T u[kBwdCh][kChunk];
+  alignas(128) T dt[kBwdCh][kChunk];
+  alignas(128) T dy[kBwdCh][kChunk];
+  alignas(128) T B[N][kChunk];
+  alignas(128) T C[N][kChunk];
+  alignas(128) int32_t pos[kChunk];
+  alignas(128) float st[N][kBwdCh];
+  alignas(128) T z[kGate ? kBwdCh : 1][kChunk];
+};
+
+// Issue the cp.async copies of chunk c's raw inputs (vector path only:
+// L*isz % 16 == 0, Dn % 4 == 0, 16-byte aligned pointers).
+template <typename T, int N, bool kGate>
+PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, int dblk, int c,
+                          int s0, uint64_t* bar) {
+  constexpr int kEl = 16 / (int)sizeof(T);       // elements per 16-byte chunk
+  constexpr int kRowQ = kChunk / kEl;            // chunks per (row, chunk)
+  const int L = a.L, Dn = a.Dn, cb = c * kChunk;
+  const bool with_st = cb > s0 || (cb == 0 && a.h0 != nullptr);
+  if (a.use_tma) {  // one thread issues the chunk's bulk tensor copies
+    if (threadIdx.x == 0) {
+      constexpr uint32_t kRows = kBwdCh * kChunk * sizeof(T);
+      const uint32_t bytes = (kGate ? 4 : 3) * kRows + 2 * N * kChunk * sizeof(T) +
+                             kChunk * sizeof(int32_t) + (with_st ? N * kBwdCh * sizeof(float) : 0);
+      mbar_expect_tx(bar, bytes);
+      const int d0 = dblk * kBwdCh;
+      tma_load<3>(rw.u, &a.tm_u, bar, cb, d0, r);
+      tma_load<3>(rw.dt, &a.tm_dt, bar, cb, d0, r);
+      tma_load<3>(rw.dy, &a.tm_dy, bar, cb, d0, r);
+      if constexpr (kGate) tma_load<3>(rw.z, &a.tm_z, bar, cb, d0, r);
+      tma_load<3>(rw.B, &a.tm_B, bar, cb, 0, r);
+      tma_load<3>(rw.C, &a.tm_C, bar, cb, 0, r);
+      tma_load<2>(rw.pos, &a.tm_pos, bar, cb, r);
+      if (with_st) tma_load<4>(rw.st, &a.tm_st, bar, d0, 0, c, r);
+    }
+    return;
+  }
+  constexpr int kTx = kBwdCh * kRowQ;
+#pragma unroll
+  for (int arr = 0; arr < (kGate ? 4 : 3); ++arr) {  // u, dt, dy (, z)
+    const T* base = static_cast<const T*>(arr == 0 ? a.u : arr == 1 ? a.dt : arr == 2 ? a.dy : a.z);
+    T(*dst)[kChunk] = arr == 0 ? rw.u : arr == 1 ? rw.dt : arr == 2 ? rw.dy : rw.z;
+    for (int e = threadIdx.x; e < kTx; e += blockDim.x) {
+      const int ch = e / kRowQ, q = e % kRowQ;
+      const int d = dblk * kBwdCh + ch;
+      const int t0 = cb + q * kEl;
+      const bool ok = d < Dn && t0 < L;
+      const T* src = ok ? base + ((int64_t)r * Dn + d) * L + t0 : base;
+      cp_async16(&dst[ch][q * kEl], src, ok ? 16 : 0);
+    }
+  }
+  const T* Bp = static_cast<const T*>(a.B) + (int64_t)r * N * L;
+  const T* Cp = static_cast<const T*>(a.C) + (int64_t)r * N * L;
+  for (int e = threadIdx.x; e < 2 * N * kRowQ; e += blockDim.x) {
+    const int arr = e / (N * kRowQ), rem = e % (N * kRowQ), n = rem / kRowQ, q = rem % kRowQ;
+    const int t0 = cb + q * kEl;
+    const bool ok = t0 < L;
+    const T* src = (arr == 0 ? Bp : Cp) + (int64_t)n * L + (ok ? t0 : 0);
+    cp_async16(&(arr == 0 ? rw.B : rw.C)[n][q * kEl], src, ok ? 16 : 0);
+  }
+  for (int e = threadIdx.x; e < kChunk / 4; e += blockDim.x) {
+    const int t0 = cb + 4 * e;
+    const bool ok = t0 < L;
+    cp_async16(&rw.pos[4 * e], a.pos + (int64_t)r * L + (ok ? t0 : 0), ok ? 16 : 0);
+  }
+  if (with_st) {
+    for (int e = threadIdx.x; e < N * (kBwdCh / 4); e += blockDim.x) {
+      const int n = e / (kBwdCh / 4), q = e % (kBwdCh / 4);
+      const int d0 = dblk * kBwdCh + 4 * q;
+      const bool ok = d0 < Dn;
+      const float* src = a.states + (((int64_t)r * a.nchunk + c) * N + n) * Dn + (ok ? d0 : 0);
+      cp_async16(&rw.st[n][4 * q], src, ok ? 16 : 0);
+    }
+  }
+  cp_async_commit();
+}
 
 // ---------------------------------------------------------------------------
 // host-side helpers shared by the three translation units

@@ -32,6 +32,29 @@ def test_library_exports_every_header_symbol():
     assert b"sm_100a" in L.pm_version()
 
 
+def header_param_counts():
+    src = open(os.path.join(ROOT, "include", "pm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    out = {}
+    for m in re.finditer(r"PM_API\s+[\w\s\*]+?\b(pm_[a-z0-9_]+)\s*\(([^)]*)\)", src):
+        args = m.group(2).strip()
+        out[m.group(1)] = 0 if args in ("", "void") else args.count(",") + 1
+    return out
+
+
+def test_binding_argtypes_match_header():
+    """Every ctypes prototype of the binding has exactly the header's number
+    of parameters (a wrong count shifts every later argument)."""
+    L = pm.lib()
+    counts = header_param_counts()
+    assert sorted(counts) == header_symbols()
+    for name, n in counts.items():
+        at = getattr(L, name).argtypes
+        if n == 0:
+            continue
+        assert at is not None and len(at) == n, (name, n, at and len(at))
+
+
 def test_library_is_sm100a_only():
     import subprocess
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", pm.LIB_PATH],

@@ -39,10 +39,15 @@ def build(cfg, R=None, seed_rows=None):
 
 
 def chain(pos, T, P):
+    """The bench's step: conv fwd, the fused scan fwd+bwd call, conv bwd."""
     u = pm.pm_causal_conv1d_fwd(T["x"], P["w"], P["bias"], pos)
-    y, st = pm.pm_selective_scan_fwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos)
-    g = pm.pm_selective_scan_bwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos,
-                                 T["dy"], states=st)
+    R, Dn, L = u.shape
+    st = torch.empty(pm.pm_selective_scan_state_bytes(R, Dn, L, P["A"].shape[1]) // 4,
+                     dtype=torch.float32, device="cuda")
+    y = torch.empty_like(u)
+    _, g = pm.pm_selective_scan_fwd_bwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
+                                        pos, T["dy"], st, out=y)
+    del st
     dx, dw, db = pm.pm_causal_conv1d_bwd(T["x"], P["w"], P["bias"], pos, g["du"])
     torch.cuda.synchronize()
     return dict(u=u, y=y, dx=dx, dw=dw, db=db, **g)
@@ -52,41 +57,67 @@ def row_np(t, r):
     return to_np(t[r:r + 1])
 
 
-@pytest.mark.parametrize("name,R", [("1.4b", 8), ("2.8b-16k", 8)])
-def test_fullsize_sampled_rows(monkeypatch, name, R):
+def fwd_split_env(cfg, R):
+    """The forward's lane split the library picks for a launch of R rows
+    (scan_impl.cuh fwd_throughput_bound), as a PM_FWD_SPLIT value that pins
+    the same choice on a launch of fewer rows."""
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    load = R * cfg.L * ((cfg.Dn + 127) // 128) / (nsm * 4)
+    return "1" if 10 * load >= 3 * cfg.L else "4"
+
+
+# Every BASELINE.json config at its full size, in the launch configuration
+# bench.py times (all rows of one GPU in one launch): 130m (fp32, latency-
+# bound: 4-lane split forward, serialized backward), 1.4b and 2.8b (bf16,
+# 8 x 4096), 2.8b-16k (bf16, all 64 rows x 16384 on one GPU).
+@pytest.mark.parametrize("name", ["130m", "1.4b", "2.8b", "2.8b-16k"])
+def test_fullsize_sampled_rows(monkeypatch, name):
     cfg = workload.CONFIGS[name]
+    R = cfg.R
     io = cfg.dtype
     pos_np, valid, T, P = build(cfg, R)
     pos = torch.as_tensor(pos_np, device="cuda")
     out = chain(pos, T, P)
     p = {k: to_np(v) for k, v in P.items()}
-    r = R - 1  # sampled row (last row: ends in padding)
-    pr = pos_np[r:r + 1]
-    x = row_np(T["x"], r)
-    ru = oracle.conv_fwd(x, p["w"], p["bias"], pr)
-    assert rel_err(row_np(out["u"], r), ru) <= TOL[(io, "fwd")]
-    u = row_np(out["u"], r)
-    args = (u, row_np(T["dt"], r), p["A"], row_np(T["B"], r), row_np(T["C"], r), p["D"],
-            p["dt_bias"], pr)
-    assert rel_err(row_np(out["y"], r), oracle.scan_fwd(*args)) <= TOL[(io, "fwd")]
-    g = oracle.scan_bwd(*args, row_np(T["dy"], r))
-    for k in ("du", "ddt", "dB", "dC"):
-        e = rel_err(row_np(out[k], r), g[k])
-        assert e <= TOL[(io, "bwd")], (k, e)
-    rdx, _, _ = oracle.conv_bwd(x, p["w"], p["bias"], pr, row_np(out["du"], r))
-    assert rel_err(row_np(out["dx"], r), rdx) <= TOL[(io, "bwd")]
-    # (b) properties of the full launch: dD[d] = sum_{r,t} dy * u
-    dD = (T["dy"].double() * out["u"].double()).sum(dim=(0, 2)).cpu().numpy()
+    # (a) sampled rows of the full launch (first, middle, last -- the last
+    # ends in padding), every per-token output element by element
+    for r in sorted({0, R // 2, R - 1}):
+        pr = pos_np[r:r + 1]
+        x = row_np(T["x"], r)
+        ru = oracle.conv_fwd(x, p["w"], p["bias"], pr)
+        assert rel_err(row_np(out["u"], r), ru) <= TOL[(io, "fwd")], (r, "u")
+        u = row_np(out["u"], r)
+        args = (u, row_np(T["dt"], r), p["A"], row_np(T["B"], r), row_np(T["C"], r), p["D"],
+                p["dt_bias"], pr)
+        e = rel_err(row_np(out["y"], r), oracle.scan_fwd(*args))
+        assert e <= TOL[(io, "fwd")], (r, "y", e)
+        g = oracle.scan_bwd(*args, row_np(T["dy"], r))
+        for k in ("du", "ddt", "dB", "dC"):
+            e = rel_err(row_np(out[k], r), g[k])
+            assert e <= TOL[(io, "bwd")], (r, k, e)
+        rdx, _, _ = oracle.conv_bwd(x, p["w"], p["bias"], pr, row_np(out["du"], r))
+        assert rel_err(row_np(out["dx"], r), rdx) <= TOL[(io, "bwd")], (r, "dx")
+        del g, args, u, x
+    # (b) properties of the full launch's parameter gradients, any size:
+    # dD[d] = sum_{r,t} dy u (fp64 from the launch's own tensors)
+    dD = sum((T["dy"][i].double() * out["u"][i].double()).sum(dim=1) for i in range(R))
+    dD = dD.cpu().numpy()
     assert rel_err(to_np(out["dD"]), dD) <= TOL[(io, "bwd")]
-    # (a) single-row launch: parameter gradients vs the oracle.  One row
-    # alone is a latency-bound launch, for which the library would split
-    # each channel's states over 4 lanes (y then sums in another order);
-    # pin the full launch's shape so the row's outputs must match bit for bit
-    monkeypatch.setenv("PM_FWD_SPLIT", "1")
+    # (c) the parameter gradients of one row's launch vs the oracle, in the
+    # full launch's shape (the forward's lane split pinned to the full
+    # launch's choice so the row's outputs must match it bit for bit)
+    r = R - 1
+    monkeypatch.setenv("PM_FWD_SPLIT", fwd_split_env(cfg, R))
     T1 = {k: v[r:r + 1].contiguous() for k, v in T.items()}
     o1 = chain(pos[r:r + 1].contiguous(), T1, P)
-    for k in ("du", "ddt", "dB", "dC", "y", "u"):  # same row, other rows absent
+    for k in ("du", "ddt", "dB", "dC", "y", "u", "dx"):  # same row, other rows absent
         assert torch.equal(o1[k][0], out[k][r]), k
+    del out
+    pr = pos_np[r:r + 1]
+    x = row_np(T["x"], r)
+    args = (row_np(o1["u"], 0), row_np(T["dt"], r), p["A"], row_np(T["B"], r),
+            row_np(T["C"], r), p["D"], p["dt_bias"], pr)
+    g = oracle.scan_bwd(*args, row_np(T["dy"], r))
     for k, ref in (("dA", g["dA"]), ("dD", g["dD"]), ("ddt_bias", g["ddt_bias"])):
         e = rel_err(to_np(o1[k]), ref)
         assert e <= TOL[(io, "bwd")], (k, e)
@@ -96,11 +127,12 @@ def test_fullsize_sampled_rows(monkeypatch, name, R):
 
 
 def test_programmatic_launch_overlap_is_bit_identical(monkeypatch):
-    """The scan bwd launched programmatically behind the scan fwd (it starts
-    on the SMs the fwd's last CTAs leave and waits per segment on the fwd's
-    release counts) must give exactly the results of the serialized launch
-    (PM_NO_PDL=1), on the bench's 1.4B launch, over repeated back-to-back
-    fwd/bwd pairs (schedule counters self-reset between bwd launches)."""
+    """pm_selective_scan_fwd_bwd launches the scan bwd programmatically behind
+    its own scan fwd (it starts on the SMs the fwd's last CTAs leave and
+    waits per segment on the fwd's release counts).  It must give exactly
+    the results of separate fwd and bwd calls (plain launches), on the
+    bench's 1.4B launch, over repeated back-to-back pairs (schedule counters
+    self-reset between bwd launches)."""
     cfg = workload.CONFIGS["1.4b"]
     pos_np, valid, T, P = build(cfg, cfg.R)
     pos = torch.as_tensor(pos_np, device="cuda")
@@ -112,22 +144,45 @@ def test_programmatic_launch_overlap_is_bit_identical(monkeypatch):
     ws = torch.empty(pm.pm_selective_scan_bwd_workspace(R, Dn, L, cfg.N), dtype=torch.uint8,
                      device="cuda")
     out = dict(du=torch.empty_like(u), ddt=torch.empty_like(u))
+    args = (u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos)
 
-    def pair():
-        pm.pm_selective_scan_fwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos,
-                                 y=y, states=st)
-        g = pm.pm_selective_scan_bwd(u, T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"],
-                                     pos, T["dy"], states=st, out=out, workspace=ws)
-        return {k: v.clone() for k, v in g.items()}
-
-    monkeypatch.setenv("PM_NO_PDL", "1")
-    ref = pair()
+    pm.pm_selective_scan_fwd(*args, y=y, states=st)
+    ref = {k: v.clone() for k, v in pm.pm_selective_scan_bwd(
+        *args, T["dy"], states=st, out=out, workspace=ws).items()}
     y_ref = y.clone()
     torch.cuda.synchronize()
-    monkeypatch.delenv("PM_NO_PDL")
+    monkeypatch.setenv("PM_PDL", "1")  # programmatic whatever the load heuristic says
     for _ in range(4):
-        got = pair()
+        y.zero_()
+        _, got = pm.pm_selective_scan_fwd_bwd(*args, T["dy"], st, out=y, grads=out, workspace=ws)
         torch.cuda.synchronize()
         assert torch.equal(y, y_ref)
         for k in ref:
             assert torch.equal(got[k], ref[k]), k
+
+
+def test_fwd_bwd_rejects_overlapping_buffers():
+    """The fused call lets the bwd start before the fwd ends, so a bwd output
+    overlapping a fwd output or an input is an argument error (pm.h)."""
+    cfg = workload.Shape("ov", 1, 256, 64, 16, 4, "f32")
+    rows = [[100, 156]]
+    pos_np, valid = workload.pos_from_rows(rows, cfg.L)
+    T = workload.row_tensors(torch, cfg, [0], valid, device="cuda")
+    P = workload.params(torch, cfg, device="cuda")
+    pos = torch.as_tensor(pos_np, device="cuda")
+    st = torch.empty(pm.pm_selective_scan_state_bytes(1, cfg.Dn, cfg.L, cfg.N) // 4,
+                     dtype=torch.float32, device="cuda")
+    args = (T["x"], T["dt"], P["A"], T["B"], T["C"], P["D"], P["dt_bias"], pos)
+    y = torch.empty_like(T["x"])
+    with pytest.raises(pm.PMError) as e:  # du aliases the forward output y
+        pm.pm_selective_scan_fwd_bwd(*args, T["dy"], st, out=y, grads=dict(du=y))
+    assert e.value.name == "PM_ERR_INVALID_ARG"
+    with pytest.raises(pm.PMError) as e:  # ddt aliases the input dt
+        pm.pm_selective_scan_fwd_bwd(*args, T["dy"], st, out=y, grads=dict(ddt=T["dt"]))
+    assert e.value.name == "PM_ERR_INVALID_ARG"
+    _, g = pm.pm_selective_scan_fwd_bwd(*args, T["dy"], st, out=y)
+    torch.cuda.synchronize()
+    g2 = pm.pm_selective_scan_bwd(*args, T["dy"], states=st)
+    torch.cuda.synchronize()
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias"):
+        assert torch.equal(g[k], g2[k]), k

@@ -156,9 +156,25 @@ def test_determinism():
 
 @pytest.mark.parametrize("io", ["f32", "bf16"])
 def test_integer_exact_bit_exact(io):
+    """Every sum is an integer below 2^24, exact in fp32 in any order; for
+    bf16 I/O every per-token input AND output is an integer of magnitude
+    <= 256 (exact in bf16) by construction: sequences of <= 17 slots and
+    N = 8 bound |h| <= 17, |y|, |du| <= 8*17 + 1, |ddt| <= 8*17 (A = 0 so the
+    dA/ddt carry term vanishes), |dx| <= K.  So both dtypes must match the
+    oracle bit for bit, forward and backward."""
     rng = np.random.default_rng(6)
-    R, Dn, L, N, K = 2, 40, 256, 16, 4
-    rows = layout("short", R, L, rng)
+    R, Dn, L, K = 2, 40, 256, 4
+    N = 16 if io == "f32" else 8
+    rows = []
+    for _ in range(R):
+        lens, t = [], 0
+        while True:
+            ln = int(rng.choice([1, 2, 3, 5, 8, 17]))
+            if t + ln > L:
+                break
+            lens.append(ln)
+            t += ln
+        rows.append(lens)
     pos_np, valid = workload.pos_from_rows(rows, L)
     pos = torch.as_tensor(pos_np, device="cuda")
     dt_ = DT[io]
@@ -170,7 +186,7 @@ def test_integer_exact_bit_exact(io):
     ref_u = oracle.conv_fwd(to_np(x), to_np(w), to_np(bias), pos_np, silu=False)
     assert np.array_equal(to_np(u), ref_u)
     # scan with A = 0 -> abar = ex2(0) = 1 exactly; delta = dt = 1
-    uu = ri(-2, 3, (R, Dn, L)).to(dt_)
+    uu = ri(-1, 2, (R, Dn, L)).to(dt_)
     B = ri(-1, 2, (R, N, L)).to(dt_)
     C = ri(-1, 2, (R, N, L)).to(dt_)
     dt = torch.ones((R, Dn, L), device="cuda", dtype=dt_)
@@ -179,20 +195,20 @@ def test_integer_exact_bit_exact(io):
     y, st = pm.pm_selective_scan_fwd(uu, dt, A, B, C, D, None, pos, dt_softplus=False)
     args = (to_np(uu), to_np(dt), to_np(A), to_np(B), to_np(C), to_np(D), None, pos_np)
     ry = oracle.scan_fwd(*args, softplus=False)
-    if io == "f32" or np.abs(ry).max() <= 256:
-        assert np.array_equal(to_np(y), ry)
-    if io == "f32":
-        dy = ri(-1, 2, (R, Dn, L)).float() * torch.as_tensor(valid, device="cuda")[:, None, :]
-        g = pm.pm_selective_scan_bwd(uu, dt, A, B, C, D, None, pos, dy, states=st,
-                                     dt_softplus=False)
-        rg = oracle.scan_bwd(*args, to_np(dy), softplus=False)
-        for k in ("du", "ddt", "dA", "dB", "dC", "dD"):
-            assert np.array_equal(to_np(g[k]), rg[k]), k
-        dx, dw, db = pm.pm_causal_conv1d_bwd(x.float(), w, bias, pos, dy, silu=False)
-        rdx, rdw, rdb = oracle.conv_bwd(to_np(x), to_np(w), to_np(bias), pos_np, to_np(dy),
-                                        silu=False)
-        assert np.array_equal(to_np(dx), rdx)
-        assert np.array_equal(to_np(dw), rdw) and np.array_equal(to_np(db), rdb)
+    assert np.abs(ry).max() <= 256  # by construction (docstring)
+    assert np.array_equal(to_np(y), ry)
+    dy = (ri(-1, 2, (R, Dn, L)).float() * torch.as_tensor(valid, device="cuda")[:, None, :]).to(dt_)
+    g = pm.pm_selective_scan_bwd(uu, dt, A, B, C, D, None, pos, dy, states=st, dt_softplus=False)
+    rg = oracle.scan_bwd(*args, to_np(dy), softplus=False)
+    for k in ("du", "ddt"):
+        assert np.abs(rg[k]).max() <= 256, k
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD"):
+        assert np.array_equal(to_np(g[k]), rg[k]), k
+    dx, dw, db = pm.pm_causal_conv1d_bwd(x, w, bias, pos, dy, silu=False)
+    rdx, rdw, rdb = oracle.conv_bwd(to_np(x), to_np(w), to_np(bias), pos_np, to_np(dy),
+                                    silu=False)
+    assert np.array_equal(to_np(dx), rdx)
+    assert np.array_equal(to_np(dw), rdw) and np.array_equal(to_np(db), rdb)
 
 
 # --------------------------------------------------------------------------
@@ -273,15 +289,26 @@ def test_many_rows_bucket_sorted_schedule():
 
 
 def test_tma_and_cp_async_staging_agree(monkeypatch):
-    """The backward stages its per-chunk inputs with TMA (bulk tensor copies)
-    when the vector path applies; PM_NO_TMA=1 selects cp.async.  Same
-    arithmetic, so the results are bit-identical."""
+    """The lane-pair backward stages its per-chunk inputs with TMA (bulk
+    tensor copies) when the vector path applies; PM_NO_TMA=1 selects
+    cp.async.  Same arithmetic, so the results are bit-identical."""
     rows, pos, valid, T, P = problem(2, 192, 1024, 16, 4, "edges", "bf16", seed=31)
     a = run_chain(pos, T, P)
     monkeypatch.setenv("PM_NO_TMA", "1")
     b = run_chain(pos, T, P)
     for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dx", "dw", "db"):
         assert torch.equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+@pytest.mark.parametrize("kind", ["random", "edges", "heads", "short"])
+def test_backward_stress_layouts_vs_oracle(io, kind):
+    """The backward (TMA staging, per-lane finish of each round's steps,
+    swizzled scalar rows) against the oracle with head-aligned chunk edges,
+    all-heads rows and short sequences, at N = 16."""
+    rows, pos, valid, T, P = problem(2, 128, 512, 16, 4, kind, io, seed=41)
+    out = run_chain(pos, T, P)
+    check_chain(pos, T, P, out, io)
 
 
 def test_programmatic_launch_over_split_forward_is_bit_identical(monkeypatch):

@@ -101,6 +101,7 @@ def main():
     traffic_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     tcfg = traffic.setdefault(cfg, {})
+    traffic["capture"] = f"{tag} (profiles/{tag}_ncu_summary.md)"
     for rep in reps:
         for m in read(rep):
             g = m.get
