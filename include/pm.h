@@ -325,6 +325,81 @@ PM_API pm_status pm_selective_scan_fwd_bwd(const void* u, const void* dt,
                                     int64_t L, int32_t N, pm_dtype io,
                                     pm_stream_t stream);
 
+/* ===========================================================================
+ * Context-parallel scan over cut sequences (the paper's
+ * future work: "cut long sequences into multiple parts and pass the
+ * hidden state between these parts ... parallel strategies for infinitely
+ * long sequences")
+ * ===========================================================================
+ * A sequence longer than a pack is laid out over consecutive rows; row r
+ * continues row r-1 iff pos[r,0] != 0 (its position indices keep counting:
+ * with h0 given, slot 0 is a head only when pos[r,0] == 0), or as `cont[r]`
+ * says when cont != NULL (cont[0]: row 0 continues the external state h_init).
+ * The recurrence is linear in the state entering a row, so
+ *   1. pm_selective_scan_fwd_ex with h0 = 0 (zeros, not NULL), states, h_last
+ *      and decay gives every row's LOCAL pass and its summary (decay, h_last);
+ *   2. pm_scan_chain_fwd composes the summaries along the chains into the
+ *      true state entering every row, h_in[r] = decay[r-1] h_in[r-1] +
+ *      h_last_local[r-1] (h_in[0] = h_init or 0), and the true h_last;
+ *   3. pm_selective_scan_fwd_fixup adds C_t . (prod_{i<=t} abar_i) h_in to
+ *      out over each continuing row's PREFIX (the slots before its first
+ *      head) and the same state correction to the prefix's chunk states --
+ *      no other slot changes, since a head resets the state.
+ * Backward: pm_selective_scan_dh0 gives each row's local dLoss/dh0 from its
+ * own outputs (reverse walk over the prefix), pm_scan_chain_bwd composes the
+ * cotangent of every row's h_last, G[r] = dh_last_ext[r] + dh0_local[r+1] +
+ * decay[r+1] G[r+1] when row r+1 continues row r, and
+ * pm_selective_scan_bwd_ex(h0 = h_in, states = the fixed-up states,
+ * dh_last = G) gives every gradient of the cut sequence.
+ * Across GPUs the same two composition kernels run on one summary per rank
+ * (cont != NULL, one "row" per rank): (chain_decay, h_last of its last row)
+ * forward, (chain_decay, dh_init) backward -- exchanged by one all_gather.
+ * All buffers (R,Dn,N) / (Dn,N) fp32, device memory, caller-owned. */
+
+/* h_in[r] (state entering row r), h_last[r] (true state after row r, or
+ * NULL) and chain_decay (Dn,N) = d h_last[R-1] / d h_init (or NULL) from the
+ * local summaries decay, h_last_local (R,Dn,N).  h_init (Dn,N) or NULL = 0.
+ * pos (R,L) is read only when cont == NULL (then L is its row length). */
+PM_API pm_status pm_scan_chain_fwd(const int32_t* pos, const int32_t* cont,
+                                   const float* decay, const float* h_last_local,
+                                   const float* h_init, float* h_in, float* h_last,
+                                   float* chain_decay, int64_t R, int64_t Dn,
+                                   int64_t L, int32_t N, pm_stream_t stream);
+/* dh_last[r] (R,Dn,N) = G[r], the cotangent of h_last[r] for the backward,
+ * from the rows' local dh0 (pm_selective_scan_dh0), the external cotangents
+ * dh_last_ext (R,Dn,N) or NULL, and g_end (Dn,N) or NULL: the cotangent of
+ * h_last[R-1] from beyond the last row (the next rank).  dh_init (Dn,N) or
+ * NULL receives dLoss/dh_init. */
+PM_API pm_status pm_scan_chain_bwd(const int32_t* pos, const int32_t* cont,
+                                   const float* decay, const float* dh0_local,
+                                   const float* dh_last_ext, const float* g_end,
+                                   float* dh_last, float* dh_init, int64_t R,
+                                   int64_t Dn, int64_t L, int32_t N,
+                                   pm_stream_t stream);
+/* In place on out (R,Dn,L, io dtype; out = y or y*silu(z)) and states (the
+ * forward's buffer or NULL): for every row with pos[r,0] != 0, every slot t
+ * before its first head gets out += C_t . (prod_{i<=t} abar_i) h_in[r]
+ * (x silu(z_t) with z != NULL) and every chunk checkpoint of that prefix the
+ * state correction.  Rows with pos[r,0] == 0 are not touched.  Arguments as
+ * pm_selective_scan_fwd_ex (same dt_softplus, A, dt_bias, z). */
+PM_API pm_status pm_selective_scan_fwd_fixup(const void* dt, const float* A,
+                                             const void* C, const float* dt_bias,
+                                             int32_t dt_softplus, const int32_t* pos,
+                                             const void* z, const float* h_in,
+                                             void* out, float* states, int64_t R,
+                                             int64_t Dn, int64_t L, int32_t N,
+                                             pm_dtype io, pm_stream_t stream);
+/* dh0_local (R,Dn,N) = dLoss/dh0 of each row through its own outputs only:
+ * sum over the slots t before the row's first head of
+ * prod_{i<=t} abar_i * C_t * dy_t, dy = dout (* silu(z) with z != NULL);
+ * 0 for rows with pos[r,0] == 0. */
+PM_API pm_status pm_selective_scan_dh0(const void* dt, const float* A, const void* C,
+                                       const float* dt_bias, int32_t dt_softplus,
+                                       const int32_t* pos, const void* z,
+                                       const void* dout, float* dh0_local, int64_t R,
+                                       int64_t Dn, int64_t L, int32_t N, pm_dtype io,
+                                       pm_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,8 @@ __all__ = [
     "pm_causal_conv1d_bwd_workspace", "pm_selective_scan_state_bytes",
     "pm_selective_scan_fwd", "pm_selective_scan_bwd",
     "pm_selective_scan_bwd_workspace", "pm_selective_scan_fwd_ex", "pm_selective_scan_bwd_ex",
-    "pm_selective_scan_fwd_bwd", "EXPORTED_SYMBOLS",
+    "pm_selective_scan_fwd_bwd", "pm_scan_chain_fwd", "pm_scan_chain_bwd",
+    "pm_selective_scan_fwd_fixup", "pm_selective_scan_dh0", "EXPORTED_SYMBOLS",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -37,7 +38,8 @@ EXPORTED_SYMBOLS = [
     "pm_pack_planned", "pm_causal_conv1d_fwd", "pm_causal_conv1d_bwd_workspace",
     "pm_causal_conv1d_bwd", "pm_selective_scan_state_bytes", "pm_selective_scan_fwd",
     "pm_selective_scan_bwd_workspace", "pm_selective_scan_bwd", "pm_selective_scan_fwd_ex",
-    "pm_selective_scan_bwd_ex", "pm_selective_scan_fwd_bwd",
+    "pm_selective_scan_bwd_ex", "pm_selective_scan_fwd_bwd", "pm_scan_chain_fwd",
+    "pm_scan_chain_bwd", "pm_selective_scan_fwd_fixup", "pm_selective_scan_dh0",
 ]
 
 
@@ -91,6 +93,12 @@ def lib():
                                                [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
         L.pm_selective_scan_fwd_bwd.argtypes = ([_vp] * 7 + [_i32, _i32] + [_vp] * 19 + [_sz] +
                                                 [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
+        L.pm_scan_chain_fwd.argtypes = [_vp] * 8 + [_i64, _i64, _i64, _i32, _vp]
+        L.pm_scan_chain_bwd.argtypes = [_vp] * 8 + [_i64, _i64, _i64, _i32, _vp]
+        L.pm_selective_scan_fwd_fixup.argtypes = ([_vp] * 4 + [_i32] + [_vp] * 5 +
+                                                  [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
+        L.pm_selective_scan_dh0.argtypes = ([_vp] * 4 + [_i32] + [_vp] * 4 +
+                                            [_i64, _i64, _i64, _i32, ctypes.c_int, _vp])
         for f in EXPORTED_SYMBOLS:
             if f not in ("pm_status_string", "pm_version") and not f.endswith(
                     ("_workspace", "_bytes")):
@@ -509,3 +517,88 @@ def pm_selective_scan_fwd_bwd(u, dt, A, B, C, Dskip, dt_bias, pos, dout, states,
         _ptr(o["ddt_bias"]), _ptr(o["dz"]), _ptr(o["dh0"]), _ptr(workspace), workspace.numel(),
         R, Dn, L, N, _io(u), _stream(u)), "pm_selective_scan_fwd_bwd")
     return out, o
+
+
+# ----------------------------------------------------------------------------
+# context-parallel scan pieces (NEXT-2); composed in .cp
+# ----------------------------------------------------------------------------
+
+def _rdn(R, Dn, N, dev):
+    import torch
+    return torch.empty((R, Dn, N), dtype=torch.float32, device=dev)
+
+
+def pm_scan_chain_fwd(decay, h_last_local, pos=None, cont=None, h_init=None, h_in=None,
+                      h_last=None, chain_decay=None):
+    """Compose row summaries along the chains (pm.h) -> (h_in, h_last, chain_decay)."""
+    import torch
+    R, Dn, N = decay.shape
+    _dev(decay, h_last_local, pos, cont, h_init)
+    for k, v in (("decay", decay), ("h_last_local", h_last_local)):
+        _want(v, k, torch.float32, (R, Dn, N))
+    _want(h_init, "h_init", torch.float32, (Dn, N))
+    _want(pos, "pos", torch.int32)
+    _want(cont, "cont", torch.int32, (R,))
+    if pos is not None and (pos.dim() != 2 or pos.shape[0] != R):
+        raise ValueError(f"pos: expected ({R}, L), got shape {tuple(pos.shape)}")
+    L = pos.shape[1] if pos is not None else 0
+    h_in = _rdn(R, Dn, N, decay.device) if h_in is None else h_in
+    h_last = _rdn(R, Dn, N, decay.device) if h_last is None else h_last
+    if chain_decay is None:
+        chain_decay = torch.empty((Dn, N), dtype=torch.float32, device=decay.device)
+    _dev(h_in, h_last, chain_decay)
+    _check(lib().pm_scan_chain_fwd(_ptr(pos), _ptr(cont), _ptr(decay), _ptr(h_last_local),
+                                   _ptr(h_init), _ptr(h_in), _ptr(h_last), _ptr(chain_decay), R,
+                                   Dn, L, N, _stream(decay)), "pm_scan_chain_fwd")
+    return h_in, h_last, chain_decay
+
+
+def pm_scan_chain_bwd(decay, dh0_local, pos=None, cont=None, dh_last_ext=None, g_end=None,
+                      dh_last=None, dh_init=None):
+    """Compose the cotangents of every row's h_last (pm.h) -> (dh_last, dh_init)."""
+    import torch
+    R, Dn, N = decay.shape
+    _dev(decay, dh0_local, pos, cont, dh_last_ext, g_end)
+    for k, v in (("decay", decay), ("dh0_local", dh0_local), ("dh_last_ext", dh_last_ext)):
+        _want(v, k, torch.float32, (R, Dn, N))
+    _want(g_end, "g_end", torch.float32, (Dn, N))
+    _want(pos, "pos", torch.int32)
+    _want(cont, "cont", torch.int32, (R,))
+    L = pos.shape[1] if pos is not None else 0
+    dh_last = _rdn(R, Dn, N, decay.device) if dh_last is None else dh_last
+    if dh_init is None:
+        dh_init = torch.empty((Dn, N), dtype=torch.float32, device=decay.device)
+    _dev(dh_last, dh_init)
+    _check(lib().pm_scan_chain_bwd(_ptr(pos), _ptr(cont), _ptr(decay), _ptr(dh0_local),
+                                   _ptr(dh_last_ext), _ptr(g_end), _ptr(dh_last), _ptr(dh_init),
+                                   R, Dn, L, N, _stream(decay)), "pm_scan_chain_bwd")
+    return dh_last, dh_init
+
+
+def pm_selective_scan_fwd_fixup(dt, A, C, dt_bias, pos, h_in, out, states=None, z=None,
+                                dt_softplus=True):
+    """Correct ``out`` (and ``states``) in place over the continuing prefixes (pm.h)."""
+    import torch
+    _dev(dt, A, C, dt_bias, pos, h_in, out, states, z)
+    R, Dn, L, N = _scan_args(out, dt, A, C, C, None, dt_bias, pos, z=z)
+    _want(h_in, "h_in", torch.float32, (R, Dn, N))
+    _states_ok(states, R, Dn, L, N)
+    _check(lib().pm_selective_scan_fwd_fixup(
+        _ptr(dt), _ptr(A), _ptr(C), _ptr(dt_bias), int(bool(dt_softplus)), _ptr(pos), _ptr(z),
+        _ptr(h_in), _ptr(out), _ptr(states), R, Dn, L, N, _io(out), _stream(out)),
+        "pm_selective_scan_fwd_fixup")
+    return out
+
+
+def pm_selective_scan_dh0(dt, A, C, dt_bias, pos, dout, z=None, dh0_local=None,
+                          dt_softplus=True):
+    """Each row's dLoss/dh0 through its own outputs (pm.h) -> dh0_local (R,Dn,N)."""
+    _dev(dt, A, C, dt_bias, pos, dout, z)
+    R, Dn, L, N = _scan_args(dout, dt, A, C, C, None, dt_bias, pos, z=z)
+    dh0_local = _rdn(R, Dn, N, dout.device) if dh0_local is None else dh0_local
+    _dev(dh0_local)
+    _check(lib().pm_selective_scan_dh0(
+        _ptr(dt), _ptr(A), _ptr(C), _ptr(dt_bias), int(bool(dt_softplus)), _ptr(pos), _ptr(z),
+        _ptr(dout), _ptr(dh0_local), R, Dn, L, N, _io(dout), _stream(dout)),
+        "pm_selective_scan_dh0")
+    return dh0_local
