@@ -112,12 +112,14 @@ template <> struct IO<float> {
   static PM_DEV float ld(const float* p) { return __ldg(p); }
   static PM_DEV void st(float* p, float v) { *p = v; }
   static PM_DEV float cvt(float v) { return v; }
+  static PM_DEV float from(float v) { return v; }
   static constexpr int kIsz = 4;
 };
 template <> struct IO<__nv_bfloat16> {
   static PM_DEV float ld(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
   static PM_DEV void st(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
   static PM_DEV float cvt(__nv_bfloat16 v) { return __bfloat162float(v); }
+  static PM_DEV __nv_bfloat16 from(float v) { return __float2bfloat16_rn(v); }
   static constexpr int kIsz = 2;
 };
 
@@ -468,6 +470,17 @@ PM_DEV int ld_acquire(const int* p) {
 }
 // generic-proxy writes (another CTA's st.global) before async-proxy reads (TMA)
 PM_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// SM count of the current device (host; 148 if the query fails)
+inline int sm_count() {
+  int dev = 0, nsm = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();  // clear: no device is not a launch error
+    nsm = 148;
+  }
+  return nsm;
+}
 
 // host-side error helper
 #define PM_LAUNCH_CHECK()                                     \

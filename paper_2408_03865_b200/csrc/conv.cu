@@ -64,7 +64,7 @@ struct Pos8 {
   PM_DEV void load(const int32_t* __restrict__ prow, int t0, int L) { load_pos8<kVec>(prow, t0, L, p); }
 };
 
-PM_DEV float silu_grad(float pre) {  // d/dpre [pre * sigmoid(pre)]
+PM_DEV float silu_grad(float pre) {  // d/dpre [pre * sigmoid(pre)] (fp32 path)
   const float s = sigmoidf_fast(pre);
   return s * fmaf(pre, 1.f - s, 1.f);
 }
@@ -72,58 +72,100 @@ PM_DEV float silu_grad(float pre) {  // d/dpre [pre * sigmoid(pre)]
 // ---------------------------------------------------------------------------
 // forward
 // ---------------------------------------------------------------------------
+#ifndef PM_CONV_CH  // channels per warp in the forward (they share pos and the tap decision)
+#define PM_CONV_CH 2
+#endif
+#ifndef PM_CONV_TANH  // SiLU (and its derivative) through one MUFU.TANH for bf16 I/O
+#define PM_CONV_TANH 1
+#endif
+constexpr int kConvCh = PM_CONV_CH;
+
+// x * sigmoid(x).  fp32 I/O: ex2 + rcp (max error a few ulp, the fp32
+// tolerance is 1e-4).  bf16 I/O: 0.5 x (1 + tanh(x / 2)) with tanh.approx
+// (one MUFU op; relative error ~5e-4, below half a bf16 ulp of the output).
+template <typename T>
+PM_DEV float silu_io(float v) {
+  if constexpr (sizeof(T) == 2 && PM_CONV_TANH) {
+    float t;
+    const float hv = 0.5f * v;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(hv));
+    return fmaf(hv, t, hv);
+  } else {
+    return v * sigmoidf_fast(v);
+  }
+}
+
+// A warp serves kConvCh consecutive channels of one row over the same time
+// range: per 256-step iteration the position indices are loaded and the tap
+// decision taken once for all of them.
 template <typename T, int K, bool kVec, bool kSilu>
 __global__ void __launch_bounds__(kConvThreads)
 conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                 const int32_t* __restrict__ pos, T* __restrict__ out, int Dn, int L, int tspan) {
+  constexpr int CH = kConvCh;
   const int lid = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int d = blockIdx.x * kConvWarps + wid;
-  if (d >= Dn) return;  // warp-uniform
+  const int d0 = (blockIdx.x * kConvWarps + wid) * CH;
+  if (d0 >= Dn) return;  // warp-uniform
   const int r = blockIdx.y;
   const int tb = blockIdx.z * tspan, te = min(L, tb + tspan);
-  const int64_t lane = ((int64_t)r * Dn + d) * L;
-  const T* xr = x + lane;
-  T* orow = out + lane;
   const int32_t* prow = pos + (int64_t)r * L;
-  float wk[K];
+  // channel c of the warp: d0 + c (clamped; a missing channel computes the
+  // last one again and does not store)
+  const T* xr[CH];
+  T* orow[CH];
+  bool own[CH];
+  float wk[CH][K], b[CH];
+  float carry[CH][K > 1 ? K - 1 : 1];  // x[t-o] for the first step of the next iteration (lane 0)
 #pragma unroll
-  for (int j = 0; j < K; ++j) wk[j] = __ldg(w + (int64_t)d * K + j);
-  const float b = bias ? __ldg(bias + d) : 0.f;
-  // carry[o-1] = x[t-o] for the first step of the next iteration (lane 0)
-  float carry[K > 1 ? K - 1 : 1];
+  for (int c = 0; c < CH; ++c) {
+    own[c] = d0 + c < Dn;
+    const int d = own[c] ? d0 + c : Dn - 1;
+    const int64_t lane = ((int64_t)r * Dn + d) * L;
+    xr[c] = x + lane;
+    orow[c] = out + lane;
 #pragma unroll
-  for (int o = 1; o < K; ++o) carry[o - 1] = (tb - o >= 0) ? IO<T>::ld(xr + tb - o) : 0.f;
+    for (int j = 0; j < K; ++j) wk[c][j] = __ldg(w + (int64_t)d * K + j);
+    b[c] = bias ? __ldg(bias + d) : 0.f;
+#pragma unroll
+    for (int o = 1; o < K; ++o) carry[c][o - 1] = (tb - o >= 0) ? IO<T>::ld(xr[c] + tb - o) : 0.f;
+  }
 
   // software pipeline: the next iteration's x/pos are in flight while this
   // one computes
-  Raw8<T, kVec> nx;
+  Raw8<T, kVec> nx[CH];
   Pos8<kVec> np;
-  nx.load(xr, tb + lid * kCE, te);
+#pragma unroll
+  for (int c = 0; c < CH; ++c) nx[c].load(xr[c], tb + lid * kCE, te);
   np.load(prow, tb + lid * kCE, te);
   for (int t0b = tb; t0b < te; t0b += kSpan) {
     const int t0 = t0b + lid * kCE;
-    float xv[8];
+    float xv[CH][8];
     int p[8];
-    nx.unpack(xv);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) nx[c].unpack(xv[c]);
 #pragma unroll
     for (int i = 0; i < 8; ++i) p[i] = np.p[i];
     if (t0b + kSpan < te) {
-      nx.load(xr, t0 + kSpan, te);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) nx[c].load(xr[c], t0 + kSpan, te);
       np.load(prow, t0 + kSpan, te);
     }
-    float X[K - 1 + 8];  // X[k] = x[t0 - (K-1) + k]
+    float X[CH][K - 1 + 8];  // X[c][k] = x[t0 - (K-1) + k]
 #pragma unroll
-    for (int o = 1; o < K; ++o) {
-      const float v = __shfl_up_sync(0xffffffffu, xv[8 - o], 1);
-      X[K - 1 - o] = lid == 0 ? carry[o - 1] : v;
+    for (int c = 0; c < CH; ++c) {
+#pragma unroll
+      for (int o = 1; o < K; ++o) {
+        const float v = __shfl_up_sync(0xffffffffu, xv[c][8 - o], 1);
+        X[c][K - 1 - o] = lid == 0 ? carry[c][o - 1] : v;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) X[c][K - 1 + i] = xv[c][i];
+#pragma unroll
+      for (int o = 1; o < K; ++o) carry[c][o - 1] = __shfl_sync(0xffffffffu, xv[c][8 - o], 31);
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) X[K - 1 + i] = xv[i];
-#pragma unroll
-    for (int o = 1; o < K; ++o) carry[o - 1] = __shfl_sync(0xffffffffu, xv[8 - o], 31);
-    // one decision per iteration: all 8 steps inside [tb, te) with every tap
-    // in range (the common case), all 8 steps sequence heads (e.g. padding),
-    // else per-step tap masks
+    // one decision per iteration for the warp's CH channels: all 8 steps
+    // inside [tb, te) with every tap in range (the common case), all 8 steps
+    // sequence heads (e.g. padding), else per-step tap masks
     int pmin = p[0], pmax = p[0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) {
@@ -133,33 +175,44 @@ conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
     const bool inr = t0 + 8 <= te;
     const bool full = inr && t0 >= K - 1 && pmin >= K - 1;
     const bool heads = inr && pmax == 0 && pmin == 0;
-    float yv[8];
+    float yv[CH][8];
     if (__all_sync(0xffffffffu, full)) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float pre = b;
+      for (int c = 0; c < CH; ++c) {
 #pragma unroll
-        for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
-        yv[i] = kSilu ? pre * sigmoidf_fast(pre) : pre;
+        for (int i = 0; i < 8; ++i) {
+          float pre = b[c];
+#pragma unroll
+          for (int j = 0; j < K; ++j) pre = fmaf(wk[c][j], X[c][i + j], pre);
+          yv[c][i] = kSilu ? silu_io<T>(pre) : pre;
+        }
       }
     } else if (__all_sync(0xffffffffu, heads)) {  // only the o = 0 tap survives
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float pre = fmaf(wk[K - 1], xv[i], b);
-        yv[i] = kSilu ? pre * sigmoidf_fast(pre) : pre;
+      for (int c = 0; c < CH; ++c) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float pre = fmaf(wk[c][K - 1], xv[c][i], b[c]);
+          yv[c][i] = kSilu ? silu_io<T>(pre) : pre;
+        }
       }
     } else {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const int ci = min(p[i], t0 + i);  // tap o kept iff o <= pos[t] and t - o >= 0
-        float pre = b;
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-          if (K - 1 - j <= ci) pre = fmaf(wk[j], X[i + j], pre);
-        yv[i] = kSilu ? pre * sigmoidf_fast(pre) : pre;
+        for (int c = 0; c < CH; ++c) {
+          float pre = b[c];
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+            if (K - 1 - j <= ci) pre = fmaf(wk[c][j], X[c][i + j], pre);
+          yv[c][i] = kSilu ? silu_io<T>(pre) : pre;
+        }
       }
     }
-    store8<T, kVec>(orow, t0, tb, te, yv);
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (own[c]) store8<T, kVec>(orow[c], t0, tb, te, yv[c]);
   }
 }
 
@@ -183,14 +236,36 @@ PM_DEV float dpre_at(const T* xr, const T* gr, const int32_t* prow, const float 
   return IO<T>::ld(gr + t) * (silu ? silu_grad(pre) : 1.f);
 }
 
+// d/dpre [pre * sigmoid(pre)] = s (1 + pre (1 - s)); bf16 I/O through one
+// MUFU.TANH: s = (1 + t) / 2, s (1 - s) = (1 - t^2) / 4, t = tanh(pre / 2)
+template <typename T>
+PM_DEV float silu_grad_io(float pre) {
+  if constexpr (sizeof(T) == 2 && PM_CONV_TANH) {
+    float t;
+    const float h = 0.5f * pre;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    const float sg = fmaf(0.5f, t, 0.5f);
+    return fmaf(0.5f * h, fmaf(-t, t, 1.f), sg);
+  } else {
+    return silu_grad(pre);
+  }
+}
+
 template <typename T, int K, bool kVec, bool kSilu>
 __global__ void __launch_bounds__(kConvBwdThreads)
 conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                 const int32_t* __restrict__ pos, const T* __restrict__ dout, T* __restrict__ dx,
                 float* __restrict__ ws, int Dn, int L, int tspan, int ntc) {
+  // one channel row per warp (32 lanes x 8 steps per iteration), walked in
+  // reverse (narrower lane groups per channel measured slower: DESIGN.md)
+  constexpr int G = 32;
+  constexpr int kConvChW = 1, kSpanG = kSpan;
   const int lid = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int d = blockIdx.x * kConvBwdWarps + wid;
-  if (d >= Dn) return;  // warp-uniform
+  const int c = lid / G, g = lid % G;
+  const int dw0 = (blockIdx.x * kConvBwdWarps + wid) * kConvChW;
+  if (dw0 >= Dn) return;  // warp-uniform
+  const bool own = dw0 + c < Dn;
+  const int d = own ? dw0 + c : Dn - 1;
   const int r = blockIdx.y, tc = blockIdx.z;
   const int tb = tc * tspan, te = min(L, tb + tspan);
   const int64_t lane = ((int64_t)r * Dn + d) * L;
@@ -204,76 +279,78 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
   const float b = bias ? __ldg(bias + d) : 0.f;
   constexpr int H = K > 1 ? K - 1 : 1;
 
-  // right-halo carry: dpre and pos of steps te .. te+K-2 (lane o-1 computes step te+o-1)
+  // right-halo carry: dpre and pos of steps te .. te+K-2 (lane g = o-1 of
+  // the group computes step te+o-1)
   float cdp[H];
   int cp[H];
   {
     float myd = 0.f;
     int myp = 0;
-    if (lid < K - 1 && te + lid < L) {
-      myd = dpre_at<T, K>(xr, gr, prow, wk, b, te + lid, L, kSilu ? 1 : 0);
-      myp = __ldg(prow + te + lid);
+    if (g < K - 1 && te + g < L) {
+      myd = dpre_at<T, K>(xr, gr, prow, wk, b, te + g, L, kSilu ? 1 : 0);
+      myp = __ldg(prow + te + g);
     }
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      cdp[o - 1] = __shfl_sync(0xffffffffu, myd, o - 1);
-      cp[o - 1] = __shfl_sync(0xffffffffu, myp, o - 1);
+      cdp[o - 1] = __shfl_sync(0xffffffffu, myd, o - 1, G);
+      cp[o - 1] = __shfl_sync(0xffffffffu, myp, o - 1, G);
     }
   }
   float acc_w[K], acc_b = 0.f;
 #pragma unroll
   for (int j = 0; j < K; ++j) acc_w[j] = 0.f;
 
-  const int nblk = (te - tb + kSpan - 1) / kSpan;
+  const int nblk = (te - tb + kSpanG - 1) / kSpanG;
   Raw8<T, kVec> nx, ng;
   Pos8<kVec> np;
-  // left halo of x for lane 0 (x[t0-K+1 .. t0-1]), loaded one iteration
+  // left halo of x for lane g = 0 (x[t0-K+1 .. t0-1]), loaded one iteration
   // ahead so no dependent global load sits in the loop body
   float hx[H];
   auto load_halo = [&](int t0l) {
 #pragma unroll
     for (int o = 1; o < K; ++o)
-      hx[o - 1] = (lid == 0 && t0l - o >= 0) ? IO<T>::ld(xr + t0l - o) : 0.f;
+      hx[o - 1] = (g == 0 && t0l - o >= 0) ? IO<T>::ld(xr + t0l - o) : 0.f;
   };
   {
-    const int t0 = tb + (nblk - 1) * kSpan + lid * kCE;
+    const int t0 = tb + (nblk - 1) * kSpanG + g * kCE;
     nx.load(xr, t0, te);
     ng.load(gr, t0, te);
     np.load(prow, t0, te);
-    load_halo(tb + (nblk - 1) * kSpan);
+    load_halo(tb + (nblk - 1) * kSpanG);
   }
   for (int blk = nblk - 1; blk >= 0; --blk) {
-    const int t0 = tb + blk * kSpan + lid * kCE;
+    const int t0 = tb + blk * kSpanG + g * kCE;
     float xv[8], gv[8];
     int p[8];
     nx.unpack(xv);
     ng.unpack(gv);
 #pragma unroll
     for (int i = 0; i < 8; ++i) p[i] = np.p[i];
-    // left halo of x: lane-1 (lane 0: the value prefetched last iteration)
+    // left halo of x: lane g-1 (g = 0: the value prefetched last iteration)
     float X[K - 1 + 8];
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      const float v = __shfl_up_sync(0xffffffffu, xv[8 - o], 1);
-      X[K - 1 - o] = lid == 0 ? hx[o - 1] : v;
+      const float v = __shfl_up_sync(0xffffffffu, xv[8 - o], 1, G);
+      X[K - 1 - o] = g == 0 ? hx[o - 1] : v;
     }
     if (blk > 0) {  // prefetch the earlier block and its halo
-      nx.load(xr, t0 - kSpan, te);
-      ng.load(gr, t0 - kSpan, te);
-      np.load(prow, t0 - kSpan, te);
-      load_halo(tb + (blk - 1) * kSpan);
+      nx.load(xr, t0 - kSpanG, te);
+      ng.load(gr, t0 - kSpanG, te);
+      np.load(prow, t0 - kSpanG, te);
+      load_halo(tb + (blk - 1) * kSpanG);
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) X[K - 1 + i] = xv[i];
-    // right halo of pos from lane+1 (lane 31: carry)
+    // right halo of pos from lane g+1 (g = G-1: carry)
     int ph[H];
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      const int vp = __shfl_down_sync(0xffffffffu, p[o - 1], 1);
-      ph[o - 1] = lid == 31 ? cp[o - 1] : vp;
+      const int vp = __shfl_down_sync(0xffffffffu, p[o - 1], 1, G);
+      ph[o - 1] = g == G - 1 ? cp[o - 1] : vp;
     }
-    // one decision per iteration: every forward tap and every dx tap valid,
-    // all 8 steps inside the range (the common case), else per-tap predicates
+    // one decision per warp iteration: every forward tap and every dx tap
+    // valid, all 8 steps inside the range (the common case), else per-tap
+    // predicates
     int pmin = p[0], pmax = p[0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) {
@@ -298,7 +375,7 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         const float pre = fmaf(wk[K - 1], xv[i], b);
-        const float dpv = gv[i] * (kSilu ? silu_grad(pre) : 1.f);
+        const float dpv = gv[i] * (kSilu ? silu_grad_io<T>(pre) : 1.f);
         dp[i] = dpv;
         acc_b += dpv;
         acc_w[K - 1] = fmaf(dpv, xv[i], acc_w[K - 1]);
@@ -310,7 +387,7 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
         float pre = b;
 #pragma unroll
         for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
-        const float dpv = gv[i] * (kSilu ? silu_grad(pre) : 1.f);
+        const float dpv = gv[i] * (kSilu ? silu_grad_io<T>(pre) : 1.f);
         dp[i] = dpv;
         acc_b += dpv;
 #pragma unroll
@@ -318,8 +395,8 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
       }
 #pragma unroll
       for (int o = 1; o < K; ++o) {
-        const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1);
-        dp[8 + o - 1] = lid == 31 ? cdp[o - 1] : vd;
+        const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1, G);
+        dp[8 + o - 1] = g == G - 1 ? cdp[o - 1] : vd;
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -337,7 +414,7 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
 #pragma unroll
         for (int j = 0; j < K; ++j)
           if (K - 1 - j <= ci) pre = fmaf(wk[j], X[i + j], pre);
-        const float dpv = (t < te) ? gv[i] * (kSilu ? silu_grad(pre) : 1.f) : 0.f;
+        const float dpv = (t < te) ? gv[i] * (kSilu ? silu_grad_io<T>(pre) : 1.f) : 0.f;
         dp[i] = dpv;
         acc_b += dpv;
 #pragma unroll
@@ -346,8 +423,8 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
       }
 #pragma unroll
       for (int o = 1; o < K; ++o) {
-        const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1);
-        dp[8 + o - 1] = lid == 31 ? cdp[o - 1] : vd;
+        const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1, G);
+        dp[8 + o - 1] = g == G - 1 ? cdp[o - 1] : vd;
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -361,21 +438,21 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
         dxv[i] = a;
       }
     }
-    // next (earlier) iteration's carry = this block's first K-1 steps (lane 0)
+    // next (earlier) iteration's carry = this block's first K-1 steps (lane g = 0)
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      cdp[o - 1] = __shfl_sync(0xffffffffu, dp[o - 1], 0);
-      cp[o - 1] = __shfl_sync(0xffffffffu, p[o - 1], 0);
+      cdp[o - 1] = __shfl_sync(0xffffffffu, dp[o - 1], 0, G);
+      cp[o - 1] = __shfl_sync(0xffffffffu, p[o - 1], 0, G);
     }
-    store8<T, kVec>(dxr, t0, tb, te, dxv);
+    if (own) store8<T, kVec>(dxr, t0, tb, te, dxv);
   }
-  // one warp reduction of (dw, db) for this (row, time range, channel)
+  // one group reduction of (dw, db) for this (row, time range, channel)
 #pragma unroll
   for (int j = 0; j <= K; ++j) {
     float v = j < K ? acc_w[j] : acc_b;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lid == 0) ws[(((int64_t)r * ntc + tc) * Dn + d) * (K + 1) + j] = v;
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+    if (g == 0 && own) ws[(((int64_t)r * ntc + tc) * Dn + d) * (K + 1) + j] = v;
   }
 }
 
@@ -402,16 +479,20 @@ using namespace pm;
 
 // time range per CTA: whole rows when R x Dn gives enough CTAs, else split
 // (multiples of kSpan) so that ~8 waves of CTAs exist.
-int conv_tspan(int64_t R, int64_t Dn, int64_t L, int warps) {
-  const int64_t ctas = R * ((Dn + warps - 1) / warps);
-  const int64_t want = (int64_t)PM_CONV_WANT * 148 * 8;
+// (chans = channels per CTA, span = steps per warp iteration)
+int conv_tspan(int64_t R, int64_t Dn, int64_t L, int chans, int span) {
+  const int64_t ctas = R * ((Dn + chans - 1) / chans);
+  const int64_t want = (int64_t)PM_CONV_WANT * sm_count() * 8;
   int64_t nt = (want + ctas - 1) / ctas;
-  const int64_t nblk = (L + kSpan - 1) / kSpan;
+  const int64_t nblk = (L + span - 1) / span;
   nt = std::max<int64_t>(1, std::min<int64_t>(nt, nblk));
   const int64_t blk_per = (nblk + nt - 1) / nt;
-  return (int)(blk_per * kSpan);
+  return (int)(blk_per * span);
 }
 int conv_ntc(int64_t L, int tspan) { return (int)((L + tspan - 1) / tspan); }
+int bwd_tspan(int64_t R, int64_t Dn, int64_t L) {
+  return conv_tspan(R, Dn, L, kConvBwdWarps, kSpan);
+}
 
 bool a16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -432,8 +513,9 @@ bool ealigned(const void* p, pm_dtype io) {
 template <typename T, int K, bool V>
 pm_status fwd_launch(const void* x, const float* w, const float* b, const int32_t* pos, void* out,
                      int64_t R, int64_t Dn, int64_t L, int silu, cudaStream_t s) {
-  const int tspan = conv_tspan(R, Dn, L, kConvWarps);
-  dim3 grid((unsigned)((Dn + kConvWarps - 1) / kConvWarps), (unsigned)R, (unsigned)conv_ntc(L, tspan));
+  const int tspan = conv_tspan(R, Dn, L, kConvWarps * kConvCh, kSpan);
+  const int64_t per_cta = (int64_t)kConvWarps * kConvCh;
+  dim3 grid((unsigned)((Dn + per_cta - 1) / per_cta), (unsigned)R, (unsigned)conv_ntc(L, tspan));
   if (silu)
     conv_fwd_kernel<T, K, V, true><<<grid, kConvThreads, 0, s>>>(
         static_cast<const T*>(x), w, b, pos, static_cast<T*>(out), (int)Dn, (int)L, tspan);
@@ -448,8 +530,9 @@ template <typename T, int K, bool V>
 pm_status bwd_launch(const void* x, const float* w, const float* b, const int32_t* pos,
                      const void* dout, void* dx, float* dw, float* db, float* ws, int64_t R,
                      int64_t Dn, int64_t L, int silu, cudaStream_t s) {
-  const int tspan = conv_tspan(R, Dn, L, kConvBwdWarps), ntc = conv_ntc(L, tspan);
-  dim3 grid((unsigned)((Dn + kConvBwdWarps - 1) / kConvBwdWarps), (unsigned)R, (unsigned)ntc);
+  const int tspan = bwd_tspan(R, Dn, L), ntc = conv_ntc(L, tspan);
+  const int64_t per_cta = kConvBwdWarps;
+  dim3 grid((unsigned)((Dn + per_cta - 1) / per_cta), (unsigned)R, (unsigned)ntc);
   if (silu)
     conv_bwd_kernel<T, K, V, true><<<grid, kConvBwdThreads, 0, s>>>(
         static_cast<const T*>(x), w, b, pos, static_cast<const T*>(dout), static_cast<T*>(dx), ws,
@@ -514,7 +597,7 @@ pm_status pm_causal_conv1d_fwd(const void* x, const float* w, const float* bias,
 
 size_t pm_causal_conv1d_bwd_workspace(int64_t R, int64_t Dn, int64_t L, int32_t K) {
   if (R < 1 || Dn < 1 || L < 1 || K < 1 || K > 4) return 0;
-  return (size_t)R * conv_ntc(L, conv_tspan(R, Dn, L, kConvBwdWarps)) * Dn * (K + 1) * sizeof(float);
+  return (size_t)R * conv_ntc(L, bwd_tspan(R, Dn, L)) * Dn * (K + 1) * sizeof(float);
 }
 
 pm_status pm_causal_conv1d_bwd(const void* x, const float* w, const float* bias, const int32_t* pos,

@@ -741,13 +741,16 @@ pm_status launch_bwd_k(const ScanBwdArgs& a, cudaStream_t s) {
     // no memset here: the counters are zeroed by the forward's schedule
     // launch and reset by this kernel's last CTA, so the launch can follow
     // the forward kernel directly (programmatic dependent launch)
-    // resident CTAs per SM: register cap (launch bounds) and 228 KB of shared
-    // memory per SM (1 KB reserved per CTA); the occupancy API under-reports
-    // this kernel, so the grid is sized from the limits directly.
-    int dev = 0, nsm = 148;
+    // resident CTAs per SM: register cap (launch bounds) and the SM's shared
+    // memory (device query; the driver reserves some per CTA); the occupancy
+    // API under-reports this kernel (TMEM), so the grid is sized from the
+    // limits directly.
+    int dev = 0, smem_sm = 228 * 1024, resv = 1024;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int nb = std::max(1, std::min<int>(kMinB, (int)((228 * 1024) / (smem + 1024))));
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&resv, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+    const int nsm = sm_count();
+    const int nb = std::max(1, std::min<int>(kMinB, (int)(smem_sm / (smem + resv))));
     const int64_t items = (int64_t)a.n_items * n_dblk_bwd(a.Dn);
     const int g = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * nb, items));
     if (getenv("PM_DEBUG"))

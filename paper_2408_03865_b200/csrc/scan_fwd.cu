@@ -384,9 +384,8 @@ namespace {
 // persistent grid: resident CTAs on all SMs, capped by the number of items
 template <typename K>
 int persistent_grid(K kern, int threads, size_t smem, int64_t items) {
-  int dev = 0, nsm = 148, nb = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int nb = 1;
+  const int nsm = sm_count();
   const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem);
   const int64_t g = (int64_t)nsm * std::max(nb, 1);
   if (getenv("PM_DEBUG"))

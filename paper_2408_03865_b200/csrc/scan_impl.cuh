@@ -241,12 +241,6 @@ inline int n_dblk_bwd(int64_t Dn) { return (int)((Dn + kBwdCh - 1) / kBwdCh); }
 // kFwdSplit threads per channel (N/S states each) and a serialized backward.
 // PM_FWD_SPLIT=1|S overrides the choice (A/B).
 template <int N> constexpr int kFwdSplit = N >= 8 ? 4 : 2;
-inline int sm_count() {
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  return nsm;
-}
 inline bool fwd_throughput_bound(int64_t R, int64_t L, int64_t Dn) {
   const int64_t load = R * L * ((Dn + kScanThreads - 1) / kScanThreads) / ((int64_t)sm_count() * kFwdMinB);
   return 10 * load >= 3 * L;
