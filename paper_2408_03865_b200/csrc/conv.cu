@@ -216,6 +216,21 @@ conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
   }
 }
 
+// d/dpre [pre * sigmoid(pre)] = s (1 + pre (1 - s)); bf16 I/O through one
+// MUFU.TANH: s = (1 + t) / 2, s (1 - s) = (1 - t^2) / 4, t = tanh(pre / 2)
+template <typename T>
+PM_DEV float silu_grad_io(float pre) {
+  if constexpr (sizeof(T) == 2 && PM_CONV_TANH) {
+    float t;
+    const float h = 0.5f * pre;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    const float sg = fmaf(0.5f, t, 0.5f);
+    return fmaf(0.5f * h, fmaf(-t, t, 1.f), sg);
+  } else {
+    return silu_grad(pre);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // backward: march through the time range in REVERSE so the right halo (dpre
 // and pos of the next K-1 steps -- the "reverse indices") is always carried
@@ -233,22 +248,7 @@ PM_DEV float dpre_at(const T* xr, const T* gr, const int32_t* prow, const float 
     const int o = K - 1 - j;
     if (o <= pt && t - o >= 0) pre = fmaf(wk[j], IO<T>::ld(xr + t - o), pre);
   }
-  return IO<T>::ld(gr + t) * (silu ? silu_grad(pre) : 1.f);
-}
-
-// d/dpre [pre * sigmoid(pre)] = s (1 + pre (1 - s)); bf16 I/O through one
-// MUFU.TANH: s = (1 + t) / 2, s (1 - s) = (1 - t^2) / 4, t = tanh(pre / 2)
-template <typename T>
-PM_DEV float silu_grad_io(float pre) {
-  if constexpr (sizeof(T) == 2 && PM_CONV_TANH) {
-    float t;
-    const float h = 0.5f * pre;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
-    const float sg = fmaf(0.5f, t, 0.5f);
-    return fmaf(0.5f * h, fmaf(-t, t, 1.f), sg);
-  } else {
-    return silu_grad(pre);
-  }
+  return IO<T>::ld(gr + t) * (silu ? silu_grad_io<T>(pre) : 1.f);
 }
 
 template <typename T, int K, bool kVec, bool kSilu>

@@ -61,16 +61,30 @@ bool encode_bwd_maps(ScanBwdArgs& a, int N, pm_dtype io) {
   return ok;
 }
 
-// bwd workspace = dB/dC partials | param partials | counter | (recomputed states)
+// bwd workspace = dB/dC partials | param partials | counters of the time
+// split | its part lists (2 x R*nslot int4) | part summaries | (recomputed
+// states)
 size_t ws_bc_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
   return up256((size_t)n_dblk_bwd(Dn) * R * L * 2 * N * sizeof(float));
 }
 size_t ws_par_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
-  return up256((size_t)R * n_seg(L) * (N + 2) * Dn * sizeof(float));
+  return up256((size_t)R * n_slots(R, L, Dn) * (N + 2) * Dn * sizeof(float));
+}
+size_t ws_tsplit_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  return n_parts(R, L, Dn) > 1 ? 2 * list_bytes(R * n_slots(R, L, Dn)) + psum_bytes(R, Dn, L, N) : 0;
 }
 size_t bwd_ws_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N, bool recompute) {
-  return ws_bc_bytes(R, Dn, L, N) + ws_par_bytes(R, Dn, L, N) + 256 +
+  return ws_bc_bytes(R, Dn, L, N) + ws_par_bytes(R, Dn, L, N) + 256 + ws_tsplit_bytes(R, Dn, L, N) +
          (recompute ? up256(state_bytes(R, Dn, L, N)) : 0);
+}
+
+// persistent schedule of a forward whose states buffer is `states`
+void set_schedule(ScanFwdArgs& a, float* states, int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  Sched sc = sched_of(states, R, Dn, L, N);
+  a.items = sc.sorted;
+  a.counter = sc.counters;
+  a.done = sc.done;
+  a.n_items = (int)(R * n_seg(L));
 }
 
 }  // namespace
@@ -112,13 +126,8 @@ pm_status pm_selective_scan_fwd_ex(const void* u, const void* dt, const float* A
   ScanFwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, out, states, nullptr, nullptr, nullptr, 0,
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
                 z, h0, h_last, decay, zoh ? 1 : 0};
-  if (states != nullptr) {  // persistent longest-first schedule lives in the states buffer
-    Sched sc = sched_of(states, R, Dn, L, N);
-    a.items = sc.sorted;
-    a.counter = sc.counters;
-    a.done = sc.done;
-    a.n_items = (int)(R * n_seg(L));
-  }
+  if (states != nullptr)  // persistent longest-first schedule lives in the states buffer
+    set_schedule(a, states, R, Dn, L, N);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   return run_scan_fwd(a, (int)N, vec, io, s);
 }
@@ -173,17 +182,17 @@ pm_status bwd_impl(const void* u, const void* dt, const float* A, const void* B,
   w += ws_par_bytes(R, Dn, L, N);
   int* counter = reinterpret_cast<int*>(w);
   w += 256;
+  const int nparts = n_parts(R, L, Dn), nslot = n_slots(R, L, Dn);
+  int4* part_lists = nparts > 1 ? reinterpret_cast<int4*>(w) : nullptr;
+  float* psum_b = nparts > 1 ? reinterpret_cast<float*>(w + 2 * list_bytes(R * nslot)) : nullptr;
+  w += ws_tsplit_bytes(R, Dn, L, N);
   const float* stp = states;
   if (recompute) {
     float* st_ws = reinterpret_cast<float*>(w);
     ScanFwdArgs fa{u, dt, A, B, C, Dskip, dt_bias, pos, nullptr, st_ws, nullptr, nullptr, nullptr, 0,
                    (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
                    nullptr, h0, nullptr, nullptr, zoh ? 1 : 0};
-    Sched sc = sched_of(st_ws, R, Dn, L, N);
-    fa.items = sc.sorted;
-    fa.counter = sc.counters;
-    fa.done = sc.done;
-    fa.n_items = (int)(R * n_seg(L));
+    set_schedule(fa, st_ws, R, Dn, L, N);
     const bool fvec = (L * isz) % 16 == 0 && aligned16(u) && aligned16(dt) && aligned16(B) &&
                       aligned16(C);
     pm_status fs = run_scan_fwd(fa, (int)N, fvec, io, s);
@@ -194,12 +203,29 @@ pm_status bwd_impl(const void* u, const void* dt, const float* A, const void* B,
   // the length-sorted segment list, work counters and per-segment done
   // counts written by the forward pass (in the states buffer)
   const Sched sc = sched_of(const_cast<float*>(stp), R, Dn, L, N);
-  (void)counter;
   ScanBwdArgs a{u, dt, A, B, C, Dskip, dt_bias, pos, stp, dout, du, ddt, ws_bc, ws_par,
                 sc.sorted, sc.counters + 1, sc.done, (int)(R * n_seg(L)),
                 (int)R, (int)Dn, (int)L, n_seg(L), n_chunks(L), dt_softplus ? 1 : 0,
                 z, h0, dh_last, dz, dh0, zoh ? 1 : 0};
   a.pdl = pdl ? 1 : 0;
+  if (nparts > 1) {
+    // time split: own part list and work counters (in the workspace), no
+    // wait on the forward's per-segment release counts, no programmatic
+    // launch; the pre-pass writes every part's summary
+    a.items = part_lists + (list_bytes(R * nslot) / 16);  // sorted list
+    a.counter = counter;
+    a.done = nullptr;
+    a.pdl = 0;
+    a.nseg = nslot;
+    a.n_items = (int)(R * nslot);
+    a.nparts = nparts;
+    a.psum = psum_b;
+    const bool pvec = (L * isz) % 16 == 0 && aligned16(dt) && aligned16(C) && aligned16(z) &&
+                      aligned16(dout);
+    const pm_status ps = run_part_bwd_pre(a, part_lists, const_cast<int4*>(a.items), counter,
+                                          (int)N, pvec, io, s);
+    if (ps != PM_OK) return ps;
+  }
   // TMA for the per-chunk inputs when the vector path applies (row strides
   // are then multiples of 16 bytes); cp.async otherwise.  PM_NO_TMA=1 forces
   // cp.async (A/B measurements).

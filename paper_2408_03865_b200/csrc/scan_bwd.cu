@@ -190,8 +190,29 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
   float dD = 0.f, ddtb = 0.f;
 
   const int cfirst = s0 / kChunk, clast = (s1 - 1) / kChunk;
-  if constexpr (kVec) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, clast, s0, &sm.bar);
-  if (s1 == L && a.dh_last != nullptr) {  // NEXT-2: cotangent of the carried-out state
+  // a time-split part that starts inside a sequence reads the (fixed-up)
+  // checkpoint at its start (chunk-aligned by construction)
+  const bool cont0 = s0 > 0 && __ldg(a.pos + (int64_t)r * L + s0) != 0;
+  if constexpr (kVec) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, clast, s0, cont0, &sm.bar);
+  if (a.psum != nullptr && !(s1 == L && a.dh_last != nullptr)) {
+    // time split: the carry entering this part's end, composed from the
+    // summaries of the segment's following parts (dh0' = the part's own
+    // dLoss/dh0, with dh_last folded in at the row end; decay = prod abar,
+    // 0 when the part does not continue into its predecessor):
+    //   G = dh0'[p+1] + decay[p+1] (dh0'[p+2] + decay[p+2] (...))
+    const int P = a.nparts, pp0 = k % P;
+    const float* base = a.psum + ((int64_t)r * a.nseg + (k - pp0)) * 2 * N * Dn + d;
+    for (int pp = P - 1; pp > pp0; --pp) {
+      const float* ps = base + (int64_t)pp * 2 * N * Dn;
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        const float2 h0v = make_float2(ps[(int64_t)(n0 + 2 * p) * Dn], ps[(int64_t)(n0 + 2 * p + 1) * Dn]);
+        const float2 dec = make_float2(ps[(int64_t)(N + n0 + 2 * p) * Dn],
+                                       ps[(int64_t)(N + n0 + 2 * p + 1) * Dn]);
+        g[p] = ffma2(dec, g[p], h0v);
+      }
+    }
+  } else if (s1 == L && a.dh_last != nullptr) {  // NEXT-2: cotangent of the carried-out state
     const float* gp = a.dh_last + ((int64_t)r * Dn + d) * N + n0;
 #pragma unroll
     for (int p = 0; p < NP; ++p) g[p] = make_float2(__ldg(gp + 2 * p), __ldg(gp + 2 * p + 1));
@@ -270,7 +291,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
           const unsigned m = __ballot_sync(0xffffffffu, f);
           if (tid == 0) sm.hmask[0] = m;
         }
-        if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
+        if (cb > s0 || (cb == 0 && a.h0 != nullptr) || (cb == s0 && cont0)) {
 #pragma unroll
           for (int p = 0; p < NP; ++p)
             h[p] = make_float2(sm.raw.st[n0 + 2 * p][cl], sm.raw.st[n0 + 2 * p + 1][cl]);
@@ -281,7 +302,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
       } else {
         stage_bc<T, N, kChunk, false, SM::kBS>(B_r, C_r, pos_row, L, cb, sm.B, sm.C, sm.hmask,
                                       a.h0 == nullptr);
-        if (cb > s0 || (cb == 0 && a.h0 != nullptr)) {
+        if (cb > s0 || (cb == 0 && a.h0 != nullptr) || (cb == s0 && cont0)) {
           const float* st = a.states + (((int64_t)r * a.nchunk + c) * N + n0) * Dn + d;
 #pragma unroll
           for (int p = 0; p < NP; ++p)
@@ -295,7 +316,7 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
     __syncthreads();  // scalars visible; raw buffer free
     const uint32_t hmask = sm.hmask[0];  // head flags of the chunk (CTA-uniform register)
     if constexpr (kVec) {
-      if (c > cfirst) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, c - 1, s0, &sm.bar);
+      if (c > cfirst) bwd_issue_raw<T, N, kGate>(sm.raw, a, r, dblk, c - 1, s0, cont0, &sm.bar);
     }
 
     auto passes = [&](auto full_tag) {

@@ -15,7 +15,7 @@ namespace pm {
 // an atomic counter in that order (LPT), so the last items are the shortest.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) seg_plan_kernel(const int32_t* __restrict__ pos, int L,
-                                                      int nseg, int4* __restrict__ items) {
+                                                      int nseg, int P, int4* __restrict__ items) {
   // cut k (1 <= k < nseg) = first head at or after k * ceil(L / nseg), as in
   // segment_bounds(); one warp per cut, 32 positions per ballot
   __shared__ int cut[65];
@@ -46,8 +46,20 @@ __global__ void __launch_bounds__(256) seg_plan_kernel(const int32_t* __restrict
     cut[nseg] = L;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < nseg; k += blockDim.x)
-    items[r * nseg + k] = make_int4(r, k, cut[k], max(cut[k], cut[k + 1]));
+  // time split (P > 1): a segment longer than kPartLen is cut into up to P
+  // parts at chunk boundaries (slot k*P + p; unused slots are empty)
+  for (int k = threadIdx.x; k < nseg; k += blockDim.x) {
+    const int c0 = cut[k], c1 = max(cut[k], cut[k + 1]), len = c1 - c0;
+    const int np = P > 1 ? min(P, max(1, (len + kPartLen - 1) / kPartLen)) : 1;
+    int b = c0;
+    for (int p = 0; p < P; ++p) {
+      const int e = p + 1 < np ? ((c0 + (int)((int64_t)(p + 1) * len / np)) & ~(kChunk - 1))
+                               : c1;
+      const int s1 = p < np ? max(b, e) : b;
+      items[(r * nseg + k) * P + p] = make_int4(r, k * P + p, b, s1);
+      b = s1;
+    }
+  }
 }
 
 // Longest-first order of the segment list (one CTA).  n <= 4096: exact rank
@@ -412,9 +424,7 @@ pm_status launch_fwd(const ScanFwdArgs& a, cudaStream_t s) {
     Sched sc = sched_of(a.states, a.R, a.Dn, a.L, N);
     if (cudaMemsetAsync(sc.counters, 0, 256 + done_bytes(a.R, a.L), s) != cudaSuccess)
       return PM_ERR_CUDA;
-    seg_plan_kernel<<<a.R, 256, 0, s>>>(a.pos, a.L, a.nseg, sc.unsorted);
-    PM_LAUNCH_CHECK();
-    seg_sort_kernel<<<1, 1024, 0, s>>>(sc.unsorted, a.n_items, a.L, sc.sorted);
+    launch_schedule(a.pos, a.R, a.L, a.nseg, 1, sc.unsorted, sc.sorted, s);
     PM_LAUNCH_CHECK();
   }
   if (a.zoh) {
@@ -446,6 +456,13 @@ pm_status dispatch_fwd_t(const ScanFwdArgs& a, int N, bool vec, cudaStream_t s) 
 }
 
 }  // namespace
+
+// segment (and, P > 1, part) list of every row, sorted longest-first
+void launch_schedule(const int32_t* pos, int R, int L, int nseg, int P, int4* unsorted,
+                     int4* sorted, cudaStream_t s) {
+  seg_plan_kernel<<<R, 256, 0, s>>>(pos, L, nseg, P, unsorted);
+  seg_sort_kernel<<<1, 1024, 0, s>>>(unsorted, R * nseg * P, L, sorted);
+}
 
 pm_status run_scan_fwd(const ScanFwdArgs& a, int N, bool vec, pm_dtype io, cudaStream_t s) {
   return io == PM_F32 ? dispatch_fwd_t<float>(a, N, vec, s) : dispatch_fwd_t<__nv_bfloat16>(a, N, vec, s);

@@ -105,6 +105,8 @@ struct ScanBwdArgs {
   void* dz;             // (R,Dn,L) when z != NULL
   float* dh0;           // (R,Dn,N) when h0 != NULL
   int zoh;              // NEXT-4: Eq 2b discretisation of B-bar (else Euler, Q1)
+  const float* psum;    // time split: part summaries (R*nseg, 2, N, Dn) or NULL
+  int nparts;           // parts per segment (1: no time split)
   // TMA descriptors of the per-chunk inputs (vector path; use_tma = 0 falls
   // back to cp.async): (L, Dn, R) u/dt/dy/z, (L, N, R) B/C, (L, R) pos,
   // (Dn, N, nchunk, R) states
@@ -164,11 +166,13 @@ struct BwdRaw {  // raw inputs of one chunk, filled by TMA or cp.async (vector p
 // L*isz % 16 == 0, Dn % 4 == 0, 16-byte aligned pointers).
 template <typename T, int N, bool kGate>
 PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, int dblk, int c,
-                          int s0, uint64_t* bar) {
+                          int s0, bool cont0, uint64_t* bar) {
   constexpr int kEl = 16 / (int)sizeof(T);       // elements per 16-byte chunk
   constexpr int kRowQ = kChunk / kEl;            // chunks per (row, chunk)
   const int L = a.L, Dn = a.Dn, cb = c * kChunk;
-  const bool with_st = cb > s0 || (cb == 0 && a.h0 != nullptr);
+  // the chunk's start state: inside the item, or at its start when the item
+  // continues a sequence (h0 at slot 0; a time-split part inside a row)
+  const bool with_st = cb > s0 || (cb == 0 && a.h0 != nullptr) || (cb == s0 && cont0);
   if (a.use_tma) {  // one thread issues the chunk's bulk tensor copies
     if (threadIdx.x == 0) {
       constexpr uint32_t kRows = kBwdCh * kChunk * sizeof(T);
@@ -255,20 +259,45 @@ inline int fwd_split(int64_t R, int64_t L, int64_t Dn, int N) {
 // the paper's length distribution a segment is ~one sequence), <= 64.
 inline int n_seg(int64_t L) { return (int)std::max<int64_t>(1, std::min<int64_t>(64, L / 256)); }
 
+// Backward time split (latency-bound launches): a segment longer than
+// kPartLen steps is cut into up to kMaxParts parts at chunk boundaries, so the
+// longest sequence no longer sets the backward's critical path.  Every part
+// starts from the forward's checkpoint at its start; the carry entering its
+// end comes from a reverse pre-pass over the following parts (tsplit.cu, the
+// NEXT-2 context-parallel algebra applied inside a row).  PM_TSPLIT=0|1
+// overrides.  (The forward stays unsplit: its prefix fix-up measured dearer
+// than the critical path it saves -- DESIGN.md.)
+#ifndef PM_MAX_PARTS
+#define PM_MAX_PARTS 4
+#endif
+constexpr int kMaxParts = PM_MAX_PARTS;
+#ifndef PM_PART_LEN
+#define PM_PART_LEN 384
+#endif
+constexpr int kPartLen = PM_PART_LEN;
+inline int n_parts(int64_t R, int64_t L, int64_t Dn) {
+  if (const char* e = getenv("PM_TSPLIT")) return atoi(e) > 0 ? kMaxParts : 1;
+  return fwd_throughput_bound(R, L, Dn) ? 1 : kMaxParts;
+}
+// backward work items per row (segments x parts)
+inline int n_slots(int64_t R, int64_t L, int64_t Dn) { return n_seg(L) * n_parts(R, L, Dn); }
+
 // states buffer = fp32 chunk states | 256 B counters | per-segment done
 // counts | sorted segment list | unsorted segment list (the fwd writes the
-// schedule; the bwd reuses it).  counters[0]: fwd work counter; [1]: bwd
-// work counter; [2]: bwd CTAs exited (the last one resets [1] and [2], so the
-// bwd needs no memset of its own and can launch programmatically right
-// behind the fwd).  done[r*nseg+k]: fwd channels finished on segment
-// (r,k) -- a bwd item starts once its segment's count reaches Dn.
+// schedule; the bwd reuses it unless it splits segments in time).
+// counters[0]: fwd work counter; [1]: bwd work counter; [2]: bwd CTAs exited
+// (the last one resets [1] and [2], so the bwd needs no memset of its own and
+// can launch programmatically right behind the fwd).  done[r*nseg+k]: fwd
+// channels finished on segment (r,k) -- a bwd item starts once its segment's
+// count reaches Dn.
 inline size_t up256(size_t x) { return (x + 255) & ~size_t(255); }
 inline size_t states_f32_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
   return (size_t)R * n_chunks(L) * N * Dn * sizeof(float);
 }
 inline size_t done_bytes(int64_t R, int64_t L) { return up256((size_t)R * n_seg(L) * sizeof(int)); }
+inline size_t list_bytes(int64_t n) { return up256((size_t)n * 16); }
 inline size_t sched_bytes(int64_t R, int64_t L) {
-  return 256 + done_bytes(R, L) + 2 * up256((size_t)R * n_seg(L) * 16);
+  return 256 + done_bytes(R, L) + 2 * list_bytes(R * n_seg(L));
 }
 inline size_t state_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
   return up256(states_f32_bytes(R, Dn, L, N)) + sched_bytes(R, L);
@@ -286,8 +315,14 @@ inline Sched sched_of(void* states, int64_t R, int64_t Dn, int64_t L, int32_t N)
   sc.done = reinterpret_cast<int*>(b + 256);
   b += 256 + done_bytes(R, L);
   sc.sorted = reinterpret_cast<int4*>(b);
-  sc.unsorted = reinterpret_cast<int4*>(b + up256((size_t)R * n_seg(L) * 16));
+  sc.unsorted = reinterpret_cast<int4*>(b + list_bytes(R * n_seg(L)));
   return sc;
+}
+// part summaries of the backward time split: (R*nslot, 2, N, Dn) fp32,
+// {the part's local dLoss/dh0, decay = prod abar over the part}
+inline size_t psum_bytes(int64_t R, int64_t Dn, int64_t L, int32_t N) {
+  return n_parts(R, L, Dn) > 1 ? up256((size_t)R * n_slots(R, L, Dn) * 2 * N * Dn * sizeof(float))
+                               : 0;
 }
 
 inline bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -297,7 +332,8 @@ inline pm_status check_common(int64_t R, int64_t Dn, int64_t L, int32_t N, pm_dt
   if (io != PM_F32 && io != PM_BF16) return PM_ERR_DTYPE;
   if (N != 4 && N != 8 && N != 16) return PM_ERR_UNSUPPORTED;
   if (R * L >= (int64_t(1) << 31) || Dn >= (int64_t(1) << 31)) return PM_ERR_SHAPE;
-  if (R > 65535 || R * n_seg(L) * ((Dn + kBwdCh - 1) / kBwdCh) >= (int64_t(1) << 31)) return PM_ERR_SHAPE;
+  if (R > 65535 || R * n_seg(L) * kMaxParts * ((Dn + kBwdCh - 1) / kBwdCh) >= (int64_t(1) << 31))
+    return PM_ERR_SHAPE;
   return PM_OK;
 }
 
@@ -311,5 +347,13 @@ inline bool elem_aligned(const void* p, pm_dtype io) {
 pm_status run_scan_fwd(const ScanFwdArgs& a, int N, bool vec, pm_dtype io, cudaStream_t s);
 pm_status run_scan_bwd(const ScanBwdArgs& a, int N, bool vec, pm_dtype io, float* dA, float* dB,
                        float* dC, float* dD, float* ddtb, cudaStream_t s);
+// backward time split (tsplit.cu): plan the parts (unsorted/sorted lists),
+// zero the work counters, run the reverse pre-pass that writes every part's
+// summary into a.psum
+pm_status run_part_bwd_pre(const ScanBwdArgs& a, int4* unsorted, int4* sorted, int* counters,
+                           int N, bool vec, pm_dtype io, cudaStream_t s);
+// the schedule kernels (scan_fwd.cu)
+void launch_schedule(const int32_t* pos, int R, int L, int nseg, int P, int4* unsorted,
+                     int4* sorted, cudaStream_t s);
 
 }  // namespace pm

@@ -136,8 +136,20 @@ def test_validation_before_launch():
     # segment schedule (256 B counters + R*nseg int32 done counts + 2 lists of
     # R*nseg int4, each 256-B aligned)
     up = lambda x: (x + 255) // 256 * 256
-    assert L.pm_selective_scan_state_bytes(2, 8, 64, 16) == (up(2 * 4 * 16 * 8 * 4) + 256 + up(2 * 1 * 4)
-                                                             + 2 * up(2 * 1 * 16))
+    assert L.pm_selective_scan_state_bytes(2, 8, 64, 16) == (
+        up(2 * 4 * 16 * 8 * 4) + 256 + up(2 * 1 * 4) + 2 * up(2 * 1 * 16))
+    # the backward's time split (kMaxParts = 4 parts per segment) adds its
+    # part lists (2 x R*slots int4) and part summaries (R*slots, 2, N, Dn)
+    # fp32 to the workspace, and R*slots param-grad partials
+    os.environ["PM_TSPLIT"] = "0"
+    try:
+        ws0 = L.pm_selective_scan_bwd_workspace(2, 8, 64, 16, 0)
+        os.environ["PM_TSPLIT"] = "1"
+        ws1 = L.pm_selective_scan_bwd_workspace(2, 8, 64, 16, 0)
+    finally:
+        del os.environ["PM_TSPLIT"]
+    par = lambda slots: up(2 * slots * (16 + 2) * 8 * 4)
+    assert ws1 - ws0 == (par(4) - par(1)) + 2 * up(2 * 4 * 16) + up(2 * 4 * 2 * 16 * 8 * 4)
 
 
 def test_pack_query_mode_and_capacity():

@@ -125,11 +125,15 @@ def test_ext_recompute_states_equals_saved():
 
 
 @pytest.mark.parametrize("m", [16, 333, 512])
-def test_cut_row_state_passing_reproduces_uncut(m):
+def test_cut_row_state_passing_reproduces_uncut(monkeypatch, m):
     """a row cut at slot m into two rows with h_last -> h0 (and dh0 ->
     dh_last backwards) gives the uncut row's results; per-token outputs are
     bit-identical (the per-lane recurrence runs the same operations in the
     same order), per-parameter sums agree to rounding."""
+    # (the backward's time split cuts the two launches' rows at different
+    # places -- another summation order -- so it is pinned off here; it has
+    # its own parity tests below)
+    monkeypatch.setenv("PM_TSPLIT", "0")
     L = 1024
     pos, u, T, P, z, h0, dh = problem(1, 128, L, 16, "random", "f32", seed=11 + m)
     full = run_ext(pos, u, T, P, z, None, None)
@@ -227,3 +231,48 @@ def test_context_parallel_scan_over_rows():
     ro, rhl = oracle.scan_fwd_ext(*args)
     assert rel_err(cat(out), ro) <= 1e-4
     assert rel_err(to_np(hl2)[-1], rhl[0]) <= 1e-4
+
+
+# --------------------------------------------------------------------------
+# backward time split of long segments (latency-bound launches): parts
+# coupled by the NEXT-2 algebra inside a row (tsplit.cu)
+# --------------------------------------------------------------------------
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+@pytest.mark.parametrize("feat", ["base", "gate", "next2", "zoh", "gate_next2"])
+def test_time_split_parity(monkeypatch, io, feat):
+    """PM_TSPLIT=1 cuts every segment longer than 384 steps into up to 4
+    chunk-aligned parts for the backward (each part starts from the
+    forward's checkpoint; the carry entering its end comes from the reverse
+    pre-pass over the following parts): one-sequence rows and long random
+    rows, with the gate, h0 / dh_last / dh0 (NEXT-2) and ZOH, against the
+    oracle; then the same launch without the split agrees to rounding."""
+    monkeypatch.setenv("PM_TSPLIT", "1")
+    kind = "one" if feat in ("base", "next2") else "random"
+    pos, u, T, P, z, h0, dh = problem(3, 96, 2048, 16, kind, io, seed=120 + len(feat),
+                                      continued=(1,))
+    z = z if "gate" in feat else None
+    nx = "next2" in feat
+    h0_, dh_ = (h0, dh) if nx else (None, None)
+    zoh = feat == "zoh"
+    res = run_ext(pos, u, T, P, z, h0_, dh_, zoh=zoh)
+    check_ext(pos, u, T, P, z, h0_, dh_, io, res, zoh=zoh)
+    monkeypatch.setenv("PM_TSPLIT", "0")
+    ref = run_ext(pos, u, T, P, z, h0_, dh_, zoh=zoh)
+    assert torch.equal(res[0], ref[0])  # the forward is not split
+    tol = 2e-2 if io == "bf16" else 1e-4
+    for k in ("du", "ddt", "dB", "dC", "dA", "dD", "ddt_bias", "dz", "dh0"):
+        if res[2].get(k) is not None:
+            assert rel_err(to_np(res[2][k]), to_np(ref[2][k])) <= 10 * tol, k
+
+
+def test_time_split_recompute_equals_saved(monkeypatch):
+    """With the split, the recompute path (states = NULL: the library runs
+    its own forward) equals the saved-states path bit for bit."""
+    monkeypatch.setenv("PM_TSPLIT", "1")
+    pos, u, T, P, z, h0, dh = problem(3, 64, 2048, 16, "one", "f32", seed=131, continued=(0, 2))
+    a = run_ext(pos, u, T, P, z, h0, dh, states=True)
+    b = run_ext(pos, u, T, P, z, h0, dh, states=False)
+    assert torch.equal(a[0], b[0])
+    for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias", "dz", "dh0"):
+        assert torch.equal(a[2][k], b[2][k]), k

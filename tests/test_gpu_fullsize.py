@@ -60,7 +60,8 @@ def row_np(t, r):
 def fwd_split_env(cfg, R):
     """The forward's lane split the library picks for a launch of R rows
     (scan_impl.cuh fwd_throughput_bound), as a PM_FWD_SPLIT value that pins
-    the same choice on a launch of fewer rows."""
+    the same choice on a launch of fewer rows (the backward's time split,
+    PM_TSPLIT, follows the same test: on iff latency-bound)."""
     nsm = torch.cuda.get_device_properties(0).multi_processor_count
     load = R * cfg.L * ((cfg.Dn + 127) // 128) / (nsm * 4)
     return "1" if 10 * load >= 3 * cfg.L else "4"
@@ -108,6 +109,7 @@ def test_fullsize_sampled_rows(monkeypatch, name):
     # launch's choice so the row's outputs must match it bit for bit)
     r = R - 1
     monkeypatch.setenv("PM_FWD_SPLIT", fwd_split_env(cfg, R))
+    monkeypatch.setenv("PM_TSPLIT", "0" if fwd_split_env(cfg, R) == "1" else "1")
     T1 = {k: v[r:r + 1].contiguous() for k, v in T.items()}
     o1 = chain(pos[r:r + 1].contiguous(), T1, P)
     for k in ("du", "ddt", "dB", "dC", "y", "u", "dx"):  # same row, other rows absent
