@@ -92,14 +92,18 @@ scan_bwd_kernel(const __grid_constant__ ScanBwdArgs a) {
   // the chunk's per-step states live in tensor memory (one TMEM lane per
   // thread, kChunk * NH fp32 columns: 128 at N = 16, so 4 CTAs fill the
   // SM's 512 columns) instead of registers or shared memory.
-  constexpr uint32_t kTmemCols = (kChunk * NH <= 32) ? 32u : (kChunk * NH <= 64 ? 64u : 128u);
+  // (warps w and w + 4 share the TMEM lane quarter w % 4: each group of 4
+  // warps takes its own kWarpCols columns)
+  constexpr uint32_t kWarpCols = (kChunk * NH <= 32) ? 32u : (kChunk * NH <= 64 ? 64u : 128u);
+  constexpr uint32_t kTmemCols = kWarpCols * ((kBwdWarps + 3) / 4);
+  static_assert(kTmemCols <= 512, "TMEM columns per CTA");
   if (wid == 0) tmem_alloc(&sm.tmem_base, kTmemCols);
   if (tid == 32) mbar_init(&sm.bar, 1);
   uint32_t bar_phase = 0;
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tbase = sm.tmem_base + ((uint32_t)((wid & 3) * 32) << 16);
+  const uint32_t tbase = sm.tmem_base + ((uint32_t)((wid & 3) * 32) << 16) + (uint32_t)(wid >> 2) * kWarpCols;
 
   for (int iter = 0;; ++iter) {
   int r, k, dblk, s0, s1;

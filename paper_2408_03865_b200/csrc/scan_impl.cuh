@@ -48,7 +48,10 @@ constexpr int kFwdMinB = PM_FWD_MINB;  // resident fwd CTAs per SM (register cap
 #endif
 constexpr int kBwdMinB = PM_BWD_MINB;  // resident bwd CTAs per SM (register cap 128; smem fits 4)
 
-constexpr int kBwdCh = 64;                   // channels per CTA
+#ifndef PM_BWD_CH
+#define PM_BWD_CH 64
+#endif
+constexpr int kBwdCh = PM_BWD_CH;            // channels per CTA
 constexpr int kBwdThreads = 2 * kBwdCh;      // lane pair per channel
 constexpr int kBwdWarps = kBwdThreads / 32;
 constexpr int kRedStride = 32;               // float4 per transpose row (no padding)
