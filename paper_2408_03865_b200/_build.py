@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpm.so")
-SOURCES = ["pack.cu", "conv.cu", "scan.cu", "scan_fwd.cu", "scan_bwd.cu", "cp.cu", "tsplit.cu"]
+SOURCES = ["pack.cu", "conv.cu", "scan.cu", "scan_fwd.cu", "scan_bwd.cu", "scan_bwd2.cu", "cp.cu", "tsplit.cu"]
 HEADERS = ["common.cuh", "scan_impl.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -36,12 +36,12 @@ bool encode_map(CUtensorMap* m, CUtensorMapDataType type, int rank, const void* 
 }
 
 // TMA descriptors of the backward's per-chunk inputs (see ScanBwdArgs).
-bool encode_bwd_maps(ScanBwdArgs& a, int N, pm_dtype io) {
+bool encode_bwd_maps(ScanBwdArgs& a, int N, pm_dtype io, int W) {
   const CUtensorMapDataType ty = io == PM_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                               : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const cuuint64_t isz = io == PM_F32 ? 4 : 2, L = a.L, Dn = a.Dn, R = a.R;
   const cuuint64_t dtok[3] = {L, Dn, R}, stok[2] = {L * isz, L * Dn * isz};
-  const cuuint32_t btok[3] = {kChunk, kBwdCh, 1};
+  const cuuint32_t btok[3] = {kChunk, (cuuint32_t)W, 1};
   const cuuint64_t dbc[3] = {L, (cuuint64_t)N, R}, sbc[2] = {L * isz, L * N * isz};
   const cuuint32_t bbc[3] = {kChunk, (cuuint32_t)N, 1};
   const cuuint64_t dpos[2] = {L, R}, spos[1] = {L * 4};
@@ -49,7 +49,7 @@ bool encode_bwd_maps(ScanBwdArgs& a, int N, pm_dtype io) {
   const cuuint64_t nch = a.nchunk;
   const cuuint64_t dst[4] = {Dn, (cuuint64_t)N, nch, R},
                    sst[3] = {Dn * 4, Dn * N * 4, Dn * N * nch * 4};
-  const cuuint32_t bst[4] = {kBwdCh, (cuuint32_t)N, 1, 1};
+  const cuuint32_t bst[4] = {(cuuint32_t)W, (cuuint32_t)N, 1, 1};
   bool ok = encode_map(&a.tm_u, ty, 3, a.u, dtok, stok, btok) &&
             encode_map(&a.tm_dt, ty, 3, a.dt, dtok, stok, btok) &&
             encode_map(&a.tm_dy, ty, 3, a.dy, dtok, stok, btok) &&
@@ -229,8 +229,15 @@ pm_status bwd_impl(const void* u, const void* dt, const float* A, const void* B,
   // TMA for the per-chunk inputs when the vector path applies (row strides
   // are then multiples of 16 bytes); cp.async otherwise.  PM_NO_TMA=1 forces
   // cp.async (A/B measurements).
-  a.use_tma = vec && Dn % 4 == 0 && getenv("PM_NO_TMA") == nullptr &&
-              encode_bwd_maps(a, (int)N, io) ? 1 : 0;
+  // The wide backward (scan_bwd2.cu, two channels per thread) serves N = 16
+  // on the TMA path without the gate or ZOH; PM_BWD_WIDE=0 forces the
+  // one-channel-per-thread kernel (A/B).
+  const char* we = getenv("PM_BWD_WIDE");
+  const bool tma = vec && Dn % 4 == 0 && getenv("PM_NO_TMA") == nullptr;
+  a.wide = tma && N == 16 && z == nullptr && !zoh && a.items != nullptr &&
+           !(we != nullptr && atoi(we) == 0) ? 1 : 0;
+  a.use_tma = tma && encode_bwd_maps(a, (int)N, io, a.wide ? kWideCh : kBwdCh) ? 1 : 0;
+  if (!a.use_tma) a.wide = 0;
   return run_scan_bwd(a, (int)N, vec, io, dA, dB, dC, dD, ddt_bias, s);
 }
 

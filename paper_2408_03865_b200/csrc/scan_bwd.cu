@@ -814,7 +814,8 @@ template <int N>
 pm_status finalize_bwd(const ScanBwdArgs& a, float* dA, float* dB, float* dC, float* dD,
                        float* ddtb, cudaStream_t s) {
   dim3 g2((a.L + 31) / 32, a.R);
-  scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC, n_dblk_bwd(a.Dn), a.R, a.L);
+  scan_bwd_finalize_bc<N><<<g2, 256, 0, s>>>(a.ws_bc, dB, dC,
+                                             a.wide ? n_dblk_wide(a.Dn) : n_dblk_bwd(a.Dn), a.R, a.L);
   PM_LAUNCH_CHECK();
   const int64_t np = (int64_t)(N + 2) * a.Dn;
   scan_bwd_finalize_param<N><<<(unsigned)((np + 31) / 32), 256, 0, s>>>(
@@ -856,6 +857,11 @@ pm_status dispatch_bwd_t(const ScanBwdArgs& a, int N, bool vec, float* dA, float
 
 pm_status run_scan_bwd(const ScanBwdArgs& a, int N, bool vec, pm_dtype io, float* dA, float* dB,
                        float* dC, float* dD, float* ddtb, cudaStream_t s) {
+  if (a.wide) {  // scan_bwd2.cu (N = 16, TMA, no gate / ZOH; see wide_bwd_ok)
+    const pm_status st = launch_scan_bwd_wide(a, io, s);
+    if (st != PM_OK) return st;
+    return finalize_bwd<16>(a, dA, dB, dC, dD, ddtb, s);
+  }
   return io == PM_F32 ? dispatch_bwd_t<float>(a, N, vec, dA, dB, dC, dD, ddtb, s)
                       : dispatch_bwd_t<__nv_bfloat16>(a, N, vec, dA, dB, dC, dD, ddtb, s);
 }

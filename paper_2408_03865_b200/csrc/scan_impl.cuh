@@ -115,6 +115,7 @@ struct ScanBwdArgs {
   // (Dn, N, nchunk, R) states
   int use_tma;
   int pdl;  // launched programmatically behind the library's own forward (pm.h)
+  int wide; // scan_bwd2.cu's two-channels-per-thread kernel (TMA maps boxed for kWideCh)
   CUtensorMap tm_u, tm_dt, tm_dy, tm_z, tm_B, tm_C, tm_pos, tm_st;
 };
 
@@ -240,6 +241,9 @@ PM_DEV void bwd_issue_raw(BwdRaw<T, N, kGate>& rw, const ScanBwdArgs& a, int r, 
 inline int n_chunks(int64_t L) { return (int)((L + kChunk - 1) / kChunk); }
 inline int n_dblk(int64_t Dn) { return (int)((Dn + kScanThreads - 1) / kScanThreads); }
 inline int n_dblk_bwd(int64_t Dn) { return (int)((Dn + kBwdCh - 1) / kBwdCh); }
+// the wide backward (scan_bwd2.cu): 128 channels per CTA, two per thread
+constexpr int kWideCh = 128;
+inline int n_dblk_wide(int64_t Dn) { return (int)((Dn + kWideCh - 1) / kWideCh); }
 
 // Forward launch shape.  Throughput-bound when the mean load per CTA slot
 // (R*L*ceil(Dn/128) step-items over nsm*kFwdMinB slots) is >= 0.3 L: one
@@ -350,6 +354,7 @@ inline bool elem_aligned(const void* p, pm_dtype io) {
 pm_status run_scan_fwd(const ScanFwdArgs& a, int N, bool vec, pm_dtype io, cudaStream_t s);
 pm_status run_scan_bwd(const ScanBwdArgs& a, int N, bool vec, pm_dtype io, float* dA, float* dB,
                        float* dC, float* dD, float* ddtb, cudaStream_t s);
+pm_status launch_scan_bwd_wide(const ScanBwdArgs& a, pm_dtype io, cudaStream_t s);
 // backward time split (tsplit.cu): plan the parts (unsorted/sorted lists),
 // zero the work counters, run the reverse pre-pass that writes every part's
 // summary into a.psum

@@ -292,6 +292,7 @@ def test_tma_and_cp_async_staging_agree(monkeypatch):
     """The lane-pair backward stages its per-chunk inputs with TMA (bulk
     tensor copies) when the vector path applies; PM_NO_TMA=1 selects
     cp.async.  Same arithmetic, so the results are bit-identical."""
+    monkeypatch.setenv("PM_BWD_WIDE", "0")  # the wide kernel has no cp.async path
     rows, pos, valid, T, P = problem(2, 192, 1024, 16, 4, "edges", "bf16", seed=31)
     a = run_chain(pos, T, P)
     monkeypatch.setenv("PM_NO_TMA", "1")
@@ -300,15 +301,38 @@ def test_tma_and_cp_async_staging_agree(monkeypatch):
         assert torch.equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("wide", ["1", "0"])
 @pytest.mark.parametrize("io", ["f32", "bf16"])
 @pytest.mark.parametrize("kind", ["random", "edges", "heads", "short"])
-def test_backward_stress_layouts_vs_oracle(io, kind):
-    """The backward (TMA staging, per-lane finish of each round's steps,
-    swizzled scalar rows) against the oracle with head-aligned chunk edges,
-    all-heads rows and short sequences, at N = 16."""
+def test_backward_stress_layouts_vs_oracle(monkeypatch, wide, io, kind):
+    """Both backward kernels at N = 16 -- the wide one (two channels per
+    thread, scan_bwd2.cu; the default on the TMA path) and the lane-pair one
+    (PM_BWD_WIDE=0: TMA staging, per-lane finish of each round's steps,
+    swizzled scalar rows) -- against the oracle with head-aligned chunk
+    edges, all-heads rows and short sequences."""
+    monkeypatch.setenv("PM_BWD_WIDE", wide)
     rows, pos, valid, T, P = problem(2, 128, 512, 16, 4, kind, io, seed=41)
     out = run_chain(pos, T, P)
     check_chain(pos, T, P, out, io)
+
+
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+@pytest.mark.parametrize("Dn", [4, 132, 200, 388])
+def test_wide_backward_partial_channel_blocks(monkeypatch, io, Dn):
+    """The wide backward's 128-channel blocks with a ragged last block (and
+    a block of 4 channels): inactive channel pairs must contribute nothing to
+    dB/dC and write nothing.  Against the oracle, and against the lane-pair
+    kernel (same per-(t,d,n) arithmetic: du, ddt, dA agree bit for bit;
+    dB/dC sum the channels, dD/ddt_bias the steps, in another order)."""
+    rows, pos, valid, T, P = problem(2, Dn, 528, 16, 4, "random", io, seed=43 + Dn)
+    a = run_chain(pos, T, P)
+    check_chain(pos, T, P, a, io)
+    monkeypatch.setenv("PM_BWD_WIDE", "0")
+    b = run_chain(pos, T, P)
+    for k in ("du", "ddt", "dA"):
+        assert torch.equal(a[k], b[k]), k
+    for k in ("dB", "dC", "dD", "ddt_bias"):
+        torch.testing.assert_close(a[k], b[k], rtol=1e-4, atol=1e-4 * float(b[k].abs().max()))
 
 
 def test_programmatic_launch_over_split_forward_is_bit_identical(monkeypatch):
