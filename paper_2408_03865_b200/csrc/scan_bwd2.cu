@@ -31,15 +31,19 @@ constexpr int kW2MinB = 2;                 // resident CTAs per SM (TMEM: 2 x 25
 #define PM_W2_AUNROLL 4
 #endif
 #ifndef PM_W2_UNROLL  // 2-step rounds unrolled per iteration of the full-chunk reverse pass
-#define PM_W2_UNROLL 1
+#define PM_W2_UNROLL 2
 #endif
 constexpr int kW2AUnroll = PM_W2_AUNROLL;
+#ifndef PM_W2_ABPARK  // hot path parks {S_k, abar_k} of even steps instead of every state
+#define PM_W2_ABPARK 0
+#endif
+constexpr bool kAbPark = PM_W2_ABPARK;
 constexpr int kW2Unroll = PM_W2_UNROLL;
 #ifndef PM_W2_AUNROLL  // steps unrolled per iteration of the full-chunk forward recompute
 #define PM_W2_AUNROLL 4
 #endif
 #ifndef PM_W2_UNROLL  // 2-step rounds unrolled per iteration of the full-chunk reverse pass
-#define PM_W2_UNROLL 1
+#define PM_W2_UNROLL 2
 #endif
 
 template <typename T, int N>
@@ -91,6 +95,40 @@ PM_DEV void w2_issue(W2Raw<T, N>& rw, const ScanBwdArgs& a, int r, int dblk, int
   tma_load<3>(rw.C, &a.tm_C, bar, cb, 0, r);
   tma_load<2>(rw.pos, &a.tm_pos, bar, cb, r);
   if (with_st) tma_load<4>(rw.st, &a.tm_st, bar, d0, 0, c, r);
+}
+
+// Split TMEM load: issue 16 columns of my lane into r (no wait) ...
+PM_DEV void tmem_ld16_issue(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+// ... and wait for it: the registers are operands of the wait, so no use of
+// them is scheduled before it (the load is asynchronous until the wait)
+PM_DEV void tmem_ld16_wait(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
+                 "+r"(r[13]), "+r"(r[14]), "+r"(r[15]));
+}
+
+// 8-byte shared store kept as such (the compiler would merge two into a
+// 16-byte store and copy the pairs into a register quad first)
+PM_DEV void sts64(uint32_t addr, float2 v) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+PM_DEV void tmem_ld32_wait(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
+                 "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]),
+                 "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]),
+                 "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]),
+                 "+r"(r[31]));
 }
 
 template <typename T, int N>
@@ -289,195 +327,288 @@ scan_bwd_wide_kernel(const __grid_constant__ ScanBwdArgs a) {
       const uint32_t hmask = sm.hmask[0];
       if (ck > cfirst) w2_issue<T, N>(sm.raw, a, r, dblk, ck - 1, s0, cont0, &sm.bar);
 
-      // three instantiations of the two passes: the hot one (a full chunk
-      // without sequence heads: no per-step head branch, so the scheduler
-      // interleaves the MUFU exponentials with the FMA work of neighbouring
-      // steps), a full chunk with heads, and a partial chunk
-      auto passes = [&](auto full_tag, auto nohead_tag) {
-        constexpr bool kFull = decltype(full_tag)::value;
-        constexpr bool kNoHead = decltype(nohead_tag)::value;
-        // ---- pass A: forward over the chunk; the state entering step ii
-        //      is parked in TMEM columns [16 ii, 16 ii + 16) of my lane ----
-        auto stepA = [&](const int ii) {
-          const int t = cb + ii;
+      // warp transpose-reduce of a round's dB/dC terms over the warp's 16
+      // channel pairs (lane -> row, state half, column half), then park my
+      // channel's (du, ddt) of the round's steps in their consumed slots
+      auto reduce_round = [&](const int rs, const float (&fdu)[2], const float (&fddt)[2]) {
+        __syncwarp();
+        {
+          const int row = lid >> 2, rh = lid & 1, ch = (lid >> 1) & 1;
+          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (row < kRows) {
+            const float4* rp = &sm.red[wid][row][2 * ch + rh];
+            const int o = (row & 1) << 2;
+            float4 p0 = rp[0 ^ o], p1 = rp[4 ^ o], p2 = rp[8 ^ o], p3 = rp[12 ^ o];
+            float4 p4 = rp[16 ^ o], p5 = rp[20 ^ o], p6 = rp[24 ^ o], p7 = rp[28 ^ o];
+            auto lo = [](float4 v) { return make_float2(v.x, v.y); };
+            auto hi = [](float4 v) { return make_float2(v.z, v.w); };
+            const float2 sl = fadd2(fadd2(fadd2(lo(p0), lo(p1)), fadd2(lo(p2), lo(p3))),
+                                    fadd2(fadd2(lo(p4), lo(p5)), fadd2(lo(p6), lo(p7))));
+            const float2 sh = fadd2(fadd2(fadd2(hi(p0), hi(p1)), fadd2(hi(p2), hi(p3))),
+                                    fadd2(fadd2(hi(p4), hi(p5)), fadd2(hi(p6), hi(p7))));
+            acc = make_float4(sl.x, sl.y, sh.x, sh.y);
+          }
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+          acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
+          acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 2);
+          if (row < kRows && ch == 0) sm.xw[rs][wid][row][rh] = acc;
+        }
+        __syncwarp();
+        // (both lanes of a pair read the round's scalars before the sync)
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+          *reinterpret_cast<float2*>(&P0[2 * rs + i][jc0]) = make_float2(fdu[i], fddt[i]);
+      };
+      // one reverse step t = cb + ii given the state after it (hc), the state
+      // entering it (hpv) and its abar (ab; unused at a head):
+      //   g += C dy;  S += g B;  dB <- sum_c g du;  dC <- sum_c dy h_t;
+      //   g <- abar g (0 at heads);  q = g h_{t-1};  dA += delta q;  dq += A q
+      // The step's dB/dC terms go to transpose row i of the round.
+      auto bstep = [&](const int ii, const int i, const bool head, const float2 (&hc)[2][NP],
+                       const float2 (&hpv)[2][NP], const float2 (&ab)[2][NP], float& fdu,
+                       float& fddt) {
+        const float4 sv0 = P0[ii][jc0], sv1 = P1[ii][jc1];
+        const float4 sv[2] = {sv0, sv1};
+        const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
+        const float2* Ct = reinterpret_cast<const float2*>(&sm.C[ii][n0]);
+        float2 vB[NP], vC[NP], Sp[2], dqp[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float2 dux2 = f2(sv[c].x * sv[c].y), dy2 = f2(sv[c].z);
+          Sp[c] = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            g[c][p] = ffma2(Ct[p], dy2, g[c][p]);
+            Sp[c] = ffma2(g[c][p], Bt[p], Sp[c]);
+            vB[p] = c == 0 ? fmul2(g[c][p], dux2) : ffma2(g[c][p], dux2, vB[p]);
+            vC[p] = c == 0 ? fmul2(dy2, hc[c][p]) : ffma2(dy2, hc[c][p], vC[p]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float2 dl2 = f2(sv[c].x);
+          dqp[c] = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) {
+            if (head) {  // abar = 0: no carry, no dA / dq term
+              g[c][p] = make_float2(0.f, 0.f);
+            } else {
+              g[c][p] = fmul2(ab[c][p], g[c][p]);  // carry to t-1
+              const float2 q = fmul2(g[c][p], hpv[c][p]);
+              dA[c][p] = ffma2(dl2, q, dA[c][p]);
+              dqp[c] = ffma2(A2[c][p], q, dqp[c]);
+            }
+          }
+        }
+        // (two 8-byte stores per slot: the fp32x2 pairs are register pairs
+        // already, a 16-byte store would first copy them into a quad)
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+          const uint32_t slot = smem_u32(&sm.red[wid][i * kQ + q][lid]);
+          sts64(slot, q < NP / 2 ? vB[2 * q] : vC[2 * q - NP]);
+          sts64(slot + 8, q < NP / 2 ? vB[2 * q + 1] : vC[2 * q + 1 - NP]);
+        }
+        // sum_n over the pair: keep local channel 0, send local channel 1
+        const float S = (Sp[0].x + Sp[0].y) + __shfl_xor_sync(0xffffffffu, Sp[1].x + Sp[1].y, 1);
+        const float dq = (dqp[0].x + dqp[0].y) + __shfl_xor_sync(0xffffffffu, dqp[1].x + dqp[1].y, 1);
+        fdu = fmaf(Dd, sv0.z, sv0.x * S);
+        fddt = fmaf(sv0.y, S, dq * kLn2) * sv0.w;
+        dD = fmaf(sv0.z, sv0.y, dD);
+        ddtb += fddt;
+      };
+      auto abar = [&](const int ii, float2 (&ab)[2][NP]) {
+        const float d0 = P0[ii][jc0].x, d1 = P1[ii][jc1].x;
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          ab[0][p] = ex2x2(fmul2(f2(d0), A2[0][p]));
+          ab[1][p] = ex2x2(fmul2(f2(d1), A2[1][p]));
+        }
+      };
+
+      if (c0 == cb && c1 == cb + kChunk && hmask == 0u && !kAbPark) {
+        // ---- hot path: a full chunk without sequence heads: no per-step
+        // head branch, so the scheduler interleaves the MUFU exponentials
+        // with the FMA work around them.  Pass A parks the state entering
+        // every step in TMEM columns [16 ii, 16 ii + 16); pass B loads a
+        // round's second-step state during the previous round's transpose
+        // and its first-step state during the second step's arithmetic.
+#pragma unroll kW2AUnroll
+        for (int ii = 0; ii < kChunk; ++ii) {
           tmem_st<2 * NH>(tbase + (uint32_t)(ii * 2 * NH), reinterpret_cast<const float*>(h));
-          if (!kFull && (t < c0 || t >= c1)) return;  // CTA-uniform
           const float4 sv0 = P0[ii][jc0], sv1 = P1[ii][jc1];
           const float2 dl2[2] = {f2(sv0.x), f2(sv1.x)};
           const float2 dux2[2] = {f2(sv0.x * sv0.y), f2(sv1.x * sv1.y)};
           const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
-          if (!kNoHead && ((hmask >> ii) & 1u)) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int p = 0; p < NP; ++p)
+              h[c][p] = ffma2(ex2x2(fmul2(dl2[c], A2[c][p])), h[c][p], fmul2(dux2[c], Bt[p]));
+        }
+        tmem_wait_st();
+        auto unpack = [&](const uint32_t (&r)[16], float2 (&v)[2][NP]) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int p = 0; p < NP; ++p)
+              v[c][p] = make_float2(__uint_as_float(r[c * NH + 2 * p]), __uint_as_float(r[c * NH + 2 * p + 1]));
+        };
+        uint32_t pre1[16];
+        tmem_ld16_issue(tbase + (uint32_t)((kChunk - 1) * 2 * NH), pre1);
+#pragma unroll kW2Unroll
+        for (int rs = kChunk / 2 - 1; rs >= 0; --rs) {
+          const int k0 = 2 * rs;
+          float2 hp0[2][NP], hp1[2][NP], ab[2][NP];
+          uint32_t r0[16];
+          tmem_ld16_wait(pre1);
+          unpack(pre1, hp1);
+          tmem_ld16_issue(tbase + (uint32_t)(k0 * 2 * NH), r0);
+          float fdu[2], fddt[2];
+          abar(k0 + 1, ab);
+          bstep(k0 + 1, 1, false, h, hp1, ab, fdu[1], fddt[1]);
+          tmem_ld16_wait(r0);
+          unpack(r0, hp0);
+          abar(k0, ab);
+          bstep(k0, 0, false, hp1, hp0, ab, fdu[0], fddt[0]);
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int p = 0; p < NP; ++p) h[c][p] = hp0[c][p];
+          if (rs > 0) tmem_ld16_issue(tbase + (uint32_t)((k0 - 1) * 2 * NH), pre1);
+          reduce_round(rs, fdu, fddt);
+        }
+      } else if (c0 == cb && c1 == cb + kChunk && hmask == 0u) {
+        // ---- hot path: a full chunk without sequence heads.  Pass A parks,
+        // for every EVEN step k, the state entering it (S_k) and its abar_k
+        // in TMEM columns [16k, 16k+16) and [16k+16, 16k+32) -- the same 16
+        // columns per step as parking every state.  Pass B rebuilds the
+        // state entering the odd step k+1 as abar_k S_k + delta u B_k (the
+        // forward's own arithmetic: bit-identical) and takes abar_k from
+        // TMEM, so only odd steps evaluate an exponential: 1.5 instead of 2
+        // MUFU ex2 per element.  No per-step head branch, so the scheduler
+        // interleaves the exponentials with the FMA work around them.
+#pragma unroll kW2AUnroll
+        for (int ii = 0; ii < kChunk; ++ii) {
+          const float4 sv0 = P0[ii][jc0], sv1 = P1[ii][jc1];
+          const float2 dl2[2] = {f2(sv0.x), f2(sv1.x)};
+          const float2 dux2[2] = {f2(sv0.x * sv0.y), f2(sv1.x * sv1.y)};
+          const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
+          float2 ab[2][NP];
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int p = 0; p < NP; ++p) ab[c][p] = ex2x2(fmul2(dl2[c], A2[c][p]));
+          if ((ii & 1) == 0) {
+            tmem_st<2 * NH>(tbase + (uint32_t)(ii * 2 * NH), reinterpret_cast<const float*>(h));
+            tmem_st<2 * NH>(tbase + (uint32_t)((ii + 1) * 2 * NH), reinterpret_cast<const float*>(ab));
+          }
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int p = 0; p < NP; ++p) h[c][p] = ffma2(ab[c][p], h[c][p], fmul2(dux2[c], Bt[p]));
+        }
+        tmem_wait_st();
+        uint32_t pre[32];  // {S_k, abar_k} of the next round, loaded during the transposes
+        tmem_ld16_issue(tbase + (uint32_t)((kChunk - 2) * 2 * NH), *reinterpret_cast<uint32_t(*)[16]>(&pre[0]));
+        tmem_ld16_issue(tbase + (uint32_t)((kChunk - 1) * 2 * NH), *reinterpret_cast<uint32_t(*)[16]>(&pre[16]));
+        auto unpack = [&](const uint32_t* r, float2 (&v)[2][NP]) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int p = 0; p < NP; ++p)
+              v[c][p] = make_float2(__uint_as_float(r[c * NH + 2 * p]), __uint_as_float(r[c * NH + 2 * p + 1]));
+        };
+#pragma unroll kW2Unroll
+        for (int rs = kChunk / 2 - 1; rs >= 0; --rs) {
+          const int k0 = 2 * rs;  // the round's even step
+          tmem_ld32_wait(pre);
+          float2 S0[2][NP], ab0[2][NP], h1[2][NP], ab1[2][NP];
+          unpack(&pre[0], S0);
+          unpack(&pre[16], ab0);
+          {  // state entering the odd step: the forward's update of S0
+            const float4 sv0 = P0[k0][jc0], sv1 = P1[k0][jc1];
+            const float2 dux2[2] = {f2(sv0.x * sv0.y), f2(sv1.x * sv1.y)};
+            const float2* Bt = reinterpret_cast<const float2*>(&sm.B[k0][n0]);
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int p = 0; p < NP; ++p) h1[c][p] = ffma2(ab0[c][p], S0[c][p], fmul2(dux2[c], Bt[p]));
+          }
+          abar(k0 + 1, ab1);
+          float fdu[2], fddt[2];
+          bstep(k0 + 1, 1, false, h, h1, ab1, fdu[1], fddt[1]);
+          bstep(k0, 0, false, h1, S0, ab0, fdu[0], fddt[0]);
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int p = 0; p < NP; ++p) h[c][p] = S0[c][p];
+          if (rs > 0) {
+            tmem_ld16_issue(tbase + (uint32_t)((k0 - 2) * 2 * NH), *reinterpret_cast<uint32_t(*)[16]>(&pre[0]));
+            tmem_ld16_issue(tbase + (uint32_t)((k0 - 1) * 2 * NH), *reinterpret_cast<uint32_t(*)[16]>(&pre[16]));
+          }
+          reduce_round(rs, fdu, fddt);
+        }
+      } else {
+        // ---- generic path (a partial chunk, or sequence heads inside):
+        // every step's entering state parked in TMEM, per-step checks ----
+        const bool full = c0 == cb && c1 == cb + kChunk;
+#pragma unroll 1
+        for (int ii = 0; ii < kChunk; ++ii) {
+          const int t = cb + ii;
+          tmem_st<2 * NH>(tbase + (uint32_t)(ii * 2 * NH), reinterpret_cast<const float*>(h));
+          if (!full && (t < c0 || t >= c1)) continue;  // CTA-uniform
+          const float4 sv0 = P0[ii][jc0], sv1 = P1[ii][jc1];
+          const float2 dux2[2] = {f2(sv0.x * sv0.y), f2(sv1.x * sv1.y)};
+          const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
+          if ((hmask >> ii) & 1u) {  // reset: h = delta u B (a select, never 0 * h)
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
               for (int p = 0; p < NP; ++p) h[c][p] = fmul2(dux2[c], Bt[p]);
-          } else if (kNoHead) {
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-              for (int p = 0; p < NP; ++p)
-                h[c][p] = ffma2(ex2x2(fmul2(dl2[c], A2[c][p])), h[c][p], fmul2(dux2[c], Bt[p]));
           } else {
-            // every exponential of the step first (MUFU latency overlaps
-            // the B products), then the state updates
             float2 ab[2][NP];
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-              for (int p = 0; p < NP; ++p) ab[c][p] = ex2x2(fmul2(dl2[c], A2[c][p]));
+            abar(ii, ab);
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
               for (int p = 0; p < NP; ++p) h[c][p] = ffma2(ab[c][p], h[c][p], fmul2(dux2[c], Bt[p]));
           }
-        };
-        if constexpr (kFull && kNoHead) {
-#pragma unroll kW2AUnroll
-          for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
-        } else if constexpr (kFull) {
-#pragma unroll 2
-          for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
-        } else {
-#pragma unroll 1
-          for (int ii = 0; ii < kChunk; ++ii) stepA(ii);
         }
         tmem_wait_st();
-        // ---- pass B: reverse over 2-step rounds:
-        //   g += C dy;  S += g B;  dB <- sum_c g du;  dC <- sum_c dy h_t;
-        //   g <- abar g (0 at heads);  q = g h_{t-1};  dA += delta q;  dq += A q
-        auto round = [&](const int rs) {
+#pragma unroll 1
+        for (int rs = kChunk / 2 - 1; rs >= 0; --rs) {
           const int a0 = cb + 2 * rs;
           float2 hp[2][2][NP];  // [step][local channel][pair]: states entering a0, a0+1
           tmem_ld<4 * NH>(tbase + (uint32_t)(rs * 4 * NH), reinterpret_cast<float*>(hp));
-          if (!kFull && (a0 >= c1 || a0 + 2 <= c0)) {  // CTA-uniform
+          if (a0 >= c1 || a0 + 2 <= c0) {  // CTA-uniform: the round is outside the item
 #pragma unroll
             for (int c = 0; c < 2; ++c)
 #pragma unroll
               for (int p = 0; p < NP; ++p) h[c][p] = hp[0][c][p];
-            return;
+            continue;
           }
           float fdu[2], fddt[2];
 #pragma unroll
           for (int i = 1; i >= 0; --i) {
             const int t = a0 + i, ii = t - cb;
-            auto rslot = [&](int q) -> float4& { return sm.red[wid][i * kQ + q][lid]; };
-            if (!kFull && (t < c0 || t >= c1)) {  // CTA-uniform
+            if (t < c0 || t >= c1) {  // CTA-uniform
 #pragma unroll
-              for (int q = 0; q < kQ; ++q) rslot(q) = make_float4(0.f, 0.f, 0.f, 0.f);
+              for (int q = 0; q < kQ; ++q) sm.red[wid][i * kQ + q][lid] = make_float4(0.f, 0.f, 0.f, 0.f);
               fdu[i] = fddt[i] = 0.f;
               continue;
             }
-            const float4 sv0 = P0[ii][jc0], sv1 = P1[ii][jc1];
-            const float4 sv[2] = {sv0, sv1};
-            const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
-            const float2* Ct = reinterpret_cast<const float2*>(&sm.C[ii][n0]);
-            float2 vB[NP], vC[NP];
-            float2 Sp[2], dqp[2];
-            const bool head = !kNoHead && ((hmask >> ii) & 1u);
-            float2 ab[2][NP];  // abar of the step (carry), issued first
-            if (kNoHead || !head) {
-#pragma unroll
-              for (int c = 0; c < 2; ++c)
-#pragma unroll
-                for (int p = 0; p < NP; ++p) ab[c][p] = ex2x2(fmul2(f2(sv[c].x), A2[c][p]));
-            }
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              const float2 dux2 = f2(sv[c].x * sv[c].y), dy2 = f2(sv[c].z);
-              const float2(&hc)[NP] = i == 1 ? h[c] : hp[1][c];  // state after step t
-              Sp[c] = make_float2(0.f, 0.f);
-#pragma unroll
-              for (int p = 0; p < NP; ++p) {
-                g[c][p] = ffma2(Ct[p], dy2, g[c][p]);
-                Sp[c] = ffma2(g[c][p], Bt[p], Sp[c]);
-                vB[p] = c == 0 ? fmul2(g[c][p], dux2) : ffma2(g[c][p], dux2, vB[p]);
-                vC[p] = c == 0 ? fmul2(dy2, hc[p]) : ffma2(dy2, hc[p], vC[p]);
-              }
-            }
-            if (head) {  // abar = 0: no carry, no dA / dq term
-#pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                dqp[c] = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) g[c][p] = make_float2(0.f, 0.f);
-              }
-            } else {
-#pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                const float2 dl2 = f2(sv[c].x);
-                dqp[c] = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int p = 0; p < NP; ++p) {
-                  g[c][p] = fmul2(ab[c][p], g[c][p]);  // carry to t-1
-                  const float2 q = fmul2(g[c][p], hp[i][c][p]);
-                  dA[c][p] = ffma2(dl2, q, dA[c][p]);
-                  dqp[c] = ffma2(A2[c][p], q, dqp[c]);
-                }
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < kQ; ++q) {
-              const float2 lo = q < NP / 2 ? vB[2 * q] : vC[2 * q - NP];
-              const float2 hi = q < NP / 2 ? vB[2 * q + 1] : vC[2 * q + 1 - NP];
-              rslot(q) = make_float4(lo.x, lo.y, hi.x, hi.y);
-            }
-            // sum_n over the pair: keep local channel 0, send local channel 1
-            const float S = (Sp[0].x + Sp[0].y) + __shfl_xor_sync(0xffffffffu, Sp[1].x + Sp[1].y, 1);
-            const float dq = (dqp[0].x + dqp[0].y) + __shfl_xor_sync(0xffffffffu, dqp[1].x + dqp[1].y, 1);
-            fdu[i] = fmaf(Dd, sv0.z, sv0.x * S);
-            fddt[i] = fmaf(sv0.y, S, dq * kLn2) * sv0.w;
-            dD = fmaf(sv0.z, sv0.y, dD);
-            ddtb += fddt[i];
+            const bool head = (hmask >> ii) & 1u;
+            float2 ab[2][NP];
+            if (!head) abar(ii, ab);
+            bstep(ii, i, head, i == 1 ? h : hp[1], hp[i], ab, fdu[i], fddt[i]);
           }
 #pragma unroll
           for (int c = 0; c < 2; ++c)
 #pragma unroll
             for (int p = 0; p < NP; ++p) h[c][p] = hp[0][c][p];
-          // warp transpose-reduce of the round over the warp's 16 channel
-          // pairs: lane -> (row, state half, column half)
-          __syncwarp();
-          {
-            const int row = lid >> 2, rh = lid & 1, ch = (lid >> 1) & 1;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (row < kRows) {
-              const float4* rp = &sm.red[wid][row][2 * ch + rh];
-              const int o = (row & 1) << 2;
-              float4 p0 = rp[0 ^ o], p1 = rp[4 ^ o], p2 = rp[8 ^ o], p3 = rp[12 ^ o];
-              float4 p4 = rp[16 ^ o], p5 = rp[20 ^ o], p6 = rp[24 ^ o], p7 = rp[28 ^ o];
-              auto lo = [](float4 v) { return make_float2(v.x, v.y); };
-              auto hi = [](float4 v) { return make_float2(v.z, v.w); };
-              const float2 sl = fadd2(fadd2(fadd2(lo(p0), lo(p1)), fadd2(lo(p2), lo(p3))),
-                                      fadd2(fadd2(lo(p4), lo(p5)), fadd2(lo(p6), lo(p7))));
-              const float2 sh = fadd2(fadd2(fadd2(hi(p0), hi(p1)), fadd2(hi(p2), hi(p3))),
-                                      fadd2(fadd2(hi(p4), hi(p5)), fadd2(hi(p6), hi(p7))));
-              acc = make_float4(sl.x, sl.y, sh.x, sh.y);
-            }
-            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
-            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
-            acc.z += __shfl_xor_sync(0xffffffffu, acc.z, 2);
-            acc.w += __shfl_xor_sync(0xffffffffu, acc.w, 2);
-            if (row < kRows && ch == 0) sm.xw[rs][wid][row][rh] = acc;
-          }
-          __syncwarp();
-          // the round's scalars are consumed (by both lanes, before the
-          // warp sync): park my channel's (du, ddt) in its slots
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-            *reinterpret_cast<float2*>(&P0[a0 - cb + i][jc0]) = make_float2(fdu[i], fddt[i]);
-        };
-        if constexpr (kFull && kNoHead) {
-#pragma unroll kW2Unroll
-          for (int rs = kChunk / 2 - 1; rs >= 0; --rs) round(rs);
-        } else {
-#pragma unroll 1
-          for (int rs = kChunk / 2 - 1; rs >= 0; --rs) round(rs);
+          reduce_round(rs, fdu, fddt);
         }
-      };
-      if (c0 == cb && c1 == cb + kChunk) {
-        if (hmask == 0u) passes(std::true_type{}, std::true_type{});
-        else passes(std::true_type{}, std::false_type{});
-      } else {
-        passes(std::false_type{}, std::false_type{});
       }
       // ---- cross-warp sum of the chunk's dB/dC partials: one barrier ----
       __syncthreads();
