@@ -39,12 +39,6 @@ constexpr int kW2AUnroll = PM_W2_AUNROLL;
 #endif
 constexpr bool kAbPark = PM_W2_ABPARK;
 constexpr int kW2Unroll = PM_W2_UNROLL;
-#ifndef PM_W2_AUNROLL  // steps unrolled per iteration of the full-chunk forward recompute
-#define PM_W2_AUNROLL 4
-#endif
-#ifndef PM_W2_UNROLL  // 2-step rounds unrolled per iteration of the full-chunk reverse pass
-#define PM_W2_UNROLL 2
-#endif
 
 template <typename T, int N>
 struct W2Raw {  // raw inputs of one chunk, filled by TMA
