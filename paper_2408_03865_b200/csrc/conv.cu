@@ -40,6 +40,10 @@ constexpr int kConvThreads = 32 * kConvWarps;
 // the backward runs one warp per CTA: its 80-register warps then pack up to
 // 25 per SM in any mix of rows (measured: 0.282 -> 0.251 ms at the 1.4B shape)
 constexpr int kConvBwdWarps = PM_CONV_BWD_WARPS;
+#ifndef PM_CONV_BWD_CH  // channels per conv bwd warp (they share pos, halo and the tap decision)
+#define PM_CONV_BWD_CH 2
+#endif
+constexpr int kConvBwdCh = PM_CONV_BWD_CH;
 constexpr int kConvBwdThreads = 32 * kConvBwdWarps;
 constexpr int kCE = 8;                         // steps per lane per iteration
 constexpr int kSpan = 32 * kCE;                // steps per warp iteration
@@ -94,6 +98,23 @@ PM_DEV float silu_io(float v) {
     return v * sigmoidf_fast(v);
   }
 }
+
+// silu for a channel pair (packed; bf16 I/O: the same arithmetic as silu_io)
+template <typename T>
+PM_DEV float2 silu2_io(float2 v) {
+  if constexpr (sizeof(T) == 2 && PM_CONV_TANH) {
+    const float2 hv = fmul2(f2(0.5f), v);
+    float2 t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t.x) : "f"(hv.x));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t.y) : "f"(hv.y));
+    return ffma2(hv, t, hv);
+  } else {
+    return make_float2(silu_io<T>(v.x), silu_io<T>(v.y));
+  }
+}
+#ifndef PM_CONV_FWD_PACK  // full-window path of the forward as packed channel pairs
+#define PM_CONV_FWD_PACK 1
+#endif
 
 // A warp serves kConvCh consecutive channels of one row over the same time
 // range: per 256-step iteration the position indices are loaded and the tap
@@ -177,14 +198,27 @@ conv_fwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
     const bool heads = inr && pmax == 0 && pmin == 0;
     float yv[CH][8];
     if (__all_sync(0xffffffffu, full)) {
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
+      if constexpr (CH == 2 && PM_CONV_FWD_PACK) {  // the two channels as packed fp32x2 pairs
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          float pre = b[c];
+          float2 pre = make_float2(b[0], b[1]);
 #pragma unroll
-          for (int j = 0; j < K; ++j) pre = fmaf(wk[c][j], X[c][i + j], pre);
-          yv[c][i] = kSilu ? silu_io<T>(pre) : pre;
+          for (int j = 0; j < K; ++j)
+            pre = ffma2(make_float2(wk[0][j], wk[1][j]), make_float2(X[0][i + j], X[1][i + j]), pre);
+          const float2 y2 = kSilu ? silu2_io<T>(pre) : pre;
+          yv[0][i] = y2.x;
+          yv[1][i] = y2.y;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float pre = b[c];
+#pragma unroll
+            for (int j = 0; j < K; ++j) pre = fmaf(wk[c][j], X[c][i + j], pre);
+            yv[c][i] = kSilu ? silu_io<T>(pre) : pre;
+          }
         }
       }
     } else if (__all_sync(0xffffffffu, heads)) {  // only the o = 0 tap survives
@@ -251,96 +285,147 @@ PM_DEV float dpre_at(const T* xr, const T* gr, const int32_t* prow, const float 
   return IO<T>::ld(gr + t) * (silu ? silu_grad_io<T>(pre) : 1.f);
 }
 
+// silu'(pre) for a channel pair (packed fp32x2; bf16 I/O: one MUFU.TANH per
+// channel, the same arithmetic as silu_grad_io)
+template <typename T>
+PM_DEV float2 silu_grad2_io(float2 pre) {
+  if constexpr (sizeof(T) == 2 && PM_CONV_TANH) {
+    const float2 h = fmul2(f2(0.5f), pre);
+    float2 t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t.x) : "f"(h.x));
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t.y) : "f"(h.y));
+    const float2 sg = ffma2(f2(0.5f), t, f2(0.5f));
+    return ffma2(fmul2(f2(0.5f), h), ffma2(make_float2(-t.x, -t.y), t, f2(1.f)), sg);
+  } else {
+    return make_float2(silu_grad(pre.x), silu_grad(pre.y));
+  }
+}
+
+#ifndef PM_CONV_BWD_MINB  // resident conv bwd CTAs (warps) per SM the register allocation targets
+#define PM_CONV_BWD_MINB 1
+#endif
 template <typename T, int K, bool kVec, bool kSilu>
-__global__ void __launch_bounds__(kConvBwdThreads)
+__global__ void __launch_bounds__(kConvBwdThreads, PM_CONV_BWD_MINB)
 conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                 const int32_t* __restrict__ pos, const T* __restrict__ dout, T* __restrict__ dx,
                 float* __restrict__ ws, int Dn, int L, int tspan, int ntc) {
-  // one channel row per warp (32 lanes x 8 steps per iteration), walked in
-  // reverse (narrower lane groups per channel measured slower: DESIGN.md)
-  constexpr int G = 32;
-  constexpr int kConvChW = 1, kSpanG = kSpan;
-  const int lid = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int c = lid / G, g = lid % G;
-  const int dw0 = (blockIdx.x * kConvBwdWarps + wid) * kConvChW;
-  if (dw0 >= Dn) return;  // warp-uniform
-  const bool own = dw0 + c < Dn;
-  const int d = own ? dw0 + c : Dn - 1;
+  // one warp = CH consecutive channel rows of one row x (32 lanes x 8 steps)
+  // per iteration, walked in reverse; the channels share the position
+  // indices, their halo and the tap decision, and the full-window path runs
+  // the two channels as packed fp32x2 pairs (FFMA2: half the instructions,
+  // no shifted operands to build)
+  constexpr int G = 32, CH = kConvBwdCh;
+  const int g = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int d0 = (blockIdx.x * kConvBwdWarps + wid) * CH;
+  if (d0 >= Dn) return;  // warp-uniform
   const int r = blockIdx.y, tc = blockIdx.z;
   const int tb = tc * tspan, te = min(L, tb + tspan);
-  const int64_t lane = ((int64_t)r * Dn + d) * L;
-  const T* xr = x + lane;
-  const T* gr = dout + lane;
-  T* dxr = dx + lane;
   const int32_t* prow = pos + (int64_t)r * L;
-  float wk[K];
+  const T* xr[CH];
+  const T* gr[CH];
+  T* dxr[CH];
+  bool own[CH];
+  int dd[CH];
+  float wk[CH][K], b[CH];
 #pragma unroll
-  for (int j = 0; j < K; ++j) wk[j] = __ldg(w + (int64_t)d * K + j);
-  const float b = bias ? __ldg(bias + d) : 0.f;
+  for (int c = 0; c < CH; ++c) {
+    own[c] = d0 + c < Dn;
+    dd[c] = own[c] ? d0 + c : Dn - 1;
+    const int64_t lane = ((int64_t)r * Dn + dd[c]) * L;
+    xr[c] = x + lane;
+    gr[c] = dout + lane;
+    dxr[c] = dx + lane;
+#pragma unroll
+    for (int j = 0; j < K; ++j) wk[c][j] = __ldg(w + (int64_t)dd[c] * K + j);
+    b[c] = bias ? __ldg(bias + dd[c]) : 0.f;
+  }
   constexpr int H = K > 1 ? K - 1 : 1;
 
-  // right-halo carry: dpre and pos of steps te .. te+K-2 (lane g = o-1 of
-  // the group computes step te+o-1)
-  float cdp[H];
+  // right-halo carry: dpre (per channel) and pos of steps te .. te+K-2
+  // (lane g = o-1 computes step te+o-1)
+  float cdp[CH][H];
   int cp[H];
   {
-    float myd = 0.f;
+    float myd[CH];
     int myp = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) myd[c] = 0.f;
     if (g < K - 1 && te + g < L) {
-      myd = dpre_at<T, K>(xr, gr, prow, wk, b, te + g, L, kSilu ? 1 : 0);
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+        myd[c] = dpre_at<T, K>(xr[c], gr[c], prow, wk[c], b[c], te + g, L, kSilu ? 1 : 0);
       myp = __ldg(prow + te + g);
     }
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      cdp[o - 1] = __shfl_sync(0xffffffffu, myd, o - 1, G);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) cdp[c][o - 1] = __shfl_sync(0xffffffffu, myd[c], o - 1, G);
       cp[o - 1] = __shfl_sync(0xffffffffu, myp, o - 1, G);
     }
   }
-  float acc_w[K], acc_b = 0.f;
+  float acc_w[CH][K], acc_b[CH];
 #pragma unroll
-  for (int j = 0; j < K; ++j) acc_w[j] = 0.f;
+  for (int c = 0; c < CH; ++c) {
+    acc_b[c] = 0.f;
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc_w[c][j] = 0.f;
+  }
 
-  const int nblk = (te - tb + kSpanG - 1) / kSpanG;
-  Raw8<T, kVec> nx, ng;
+  const int nblk = (te - tb + kSpan - 1) / kSpan;
+  Raw8<T, kVec> nx[CH], ng[CH];
   Pos8<kVec> np;
   // left halo of x for lane g = 0 (x[t0-K+1 .. t0-1]), loaded one iteration
   // ahead so no dependent global load sits in the loop body
-  float hx[H];
+  float hx[CH][H];
   auto load_halo = [&](int t0l) {
 #pragma unroll
-    for (int o = 1; o < K; ++o)
-      hx[o - 1] = (g == 0 && t0l - o >= 0) ? IO<T>::ld(xr + t0l - o) : 0.f;
+    for (int c = 0; c < CH; ++c)
+#pragma unroll
+      for (int o = 1; o < K; ++o)
+        hx[c][o - 1] = (g == 0 && t0l - o >= 0) ? IO<T>::ld(xr[c] + t0l - o) : 0.f;
   };
   {
-    const int t0 = tb + (nblk - 1) * kSpanG + g * kCE;
-    nx.load(xr, t0, te);
-    ng.load(gr, t0, te);
+    const int t0 = tb + (nblk - 1) * kSpan + g * kCE;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      nx[c].load(xr[c], t0, te);
+      ng[c].load(gr[c], t0, te);
+    }
     np.load(prow, t0, te);
-    load_halo(tb + (nblk - 1) * kSpanG);
+    load_halo(tb + (nblk - 1) * kSpan);
   }
   for (int blk = nblk - 1; blk >= 0; --blk) {
-    const int t0 = tb + blk * kSpanG + g * kCE;
-    float xv[8], gv[8];
+    const int t0 = tb + blk * kSpan + g * kCE;
+    float xv[CH][8], gv[CH][8];
     int p[8];
-    nx.unpack(xv);
-    ng.unpack(gv);
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      nx[c].unpack(xv[c]);
+      ng[c].unpack(gv[c]);
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) p[i] = np.p[i];
     // left halo of x: lane g-1 (g = 0: the value prefetched last iteration)
-    float X[K - 1 + 8];
+    float X[CH][K - 1 + 8];
 #pragma unroll
-    for (int o = 1; o < K; ++o) {
-      const float v = __shfl_up_sync(0xffffffffu, xv[8 - o], 1, G);
-      X[K - 1 - o] = g == 0 ? hx[o - 1] : v;
+    for (int c = 0; c < CH; ++c) {
+#pragma unroll
+      for (int o = 1; o < K; ++o) {
+        const float v = __shfl_up_sync(0xffffffffu, xv[c][8 - o], 1, G);
+        X[c][K - 1 - o] = g == 0 ? hx[c][o - 1] : v;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) X[c][K - 1 + i] = xv[c][i];
     }
     if (blk > 0) {  // prefetch the earlier block and its halo
-      nx.load(xr, t0 - kSpanG, te);
-      ng.load(gr, t0 - kSpanG, te);
-      np.load(prow, t0 - kSpanG, te);
-      load_halo(tb + (blk - 1) * kSpanG);
-    }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) X[K - 1 + i] = xv[i];
+      for (int c = 0; c < CH; ++c) {
+        nx[c].load(xr[c], t0 - kSpan, te);
+        ng[c].load(gr[c], t0 - kSpan, te);
+      }
+      np.load(prow, t0 - kSpan, te);
+      load_halo(tb + (blk - 1) * kSpan);
+    }
     // right halo of pos from lane g+1 (g = G-1: carry)
     int ph[H];
 #pragma unroll
@@ -348,9 +433,9 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
       const int vp = __shfl_down_sync(0xffffffffu, p[o - 1], 1, G);
       ph[o - 1] = g == G - 1 ? cp[o - 1] : vp;
     }
-    // one decision per warp iteration: every forward tap and every dx tap
-    // valid, all 8 steps inside the range (the common case), else per-tap
-    // predicates
+    // one decision per warp iteration for all CH channels: every forward tap
+    // and every dx tap valid, all 8 steps inside the range (the common
+    // case), else per-tap predicates
     int pmin = p[0], pmax = p[0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) {
@@ -369,90 +454,150 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
     // padding run at the end of a row: only the o = 0 tap survives
     const bool heads = inr && pmax == 0 && pmin == 0;
     const bool wheads = K > 1 && !wfull && __all_sync(0xffffffffu, heads);
-    float dp[8 + H];
-    float dxv[8];
-    if (wheads) {
+    float dp[CH][8 + H];
+    float dxv[CH][8];
+    if (wfull && CH == 2) {
+      // packed: lane .x = channel d0, .y = channel d0 + 1
+      float2 X2[K - 1 + 8], w2[K], dp2[8 + H];
+#pragma unroll
+      for (int k = 0; k < K - 1 + 8; ++k) X2[k] = make_float2(X[0][k], X[CH - 1][k]);
+#pragma unroll
+      for (int j = 0; j < K; ++j) w2[j] = make_float2(wk[0][j], wk[CH - 1][j]);
+      float2 ab2 = make_float2(acc_b[0], acc_b[CH - 1]);
+      float2 aw2[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) aw2[j] = make_float2(acc_w[0][j], acc_w[CH - 1][j]);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float pre = fmaf(wk[K - 1], xv[i], b);
-        const float dpv = gv[i] * (kSilu ? silu_grad_io<T>(pre) : 1.f);
-        dp[i] = dpv;
-        acc_b += dpv;
-        acc_w[K - 1] = fmaf(dpv, xv[i], acc_w[K - 1]);
-        dxv[i] = wk[K - 1] * dpv;
-      }
-    } else if (wfull) {
+        float2 pre = make_float2(b[0], b[CH - 1]);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float pre = b;
+        for (int j = 0; j < K; ++j) pre = ffma2(w2[j], X2[i + j], pre);
+        const float2 g2 = make_float2(gv[0][i], gv[CH - 1][i]);
+        const float2 dpv = kSilu ? fmul2(g2, silu_grad2_io<T>(pre)) : g2;
+        dp2[i] = dpv;
+        ab2 = fadd2(ab2, dpv);
 #pragma unroll
-        for (int j = 0; j < K; ++j) pre = fmaf(wk[j], X[i + j], pre);
-        const float dpv = gv[i] * (kSilu ? silu_grad_io<T>(pre) : 1.f);
-        dp[i] = dpv;
-        acc_b += dpv;
-#pragma unroll
-        for (int j = 0; j < K; ++j) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
+        for (int j = 0; j < K; ++j) aw2[j] = ffma2(dpv, X2[i + j], aw2[j]);
       }
 #pragma unroll
       for (int o = 1; o < K; ++o) {
-        const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1, G);
-        dp[8 + o - 1] = g == G - 1 ? cdp[o - 1] : vd;
+        const float vx = __shfl_down_sync(0xffffffffu, dp2[o - 1].x, 1, G);
+        const float vy = __shfl_down_sync(0xffffffffu, dp2[o - 1].y, 1, G);
+        dp2[8 + o - 1] = g == G - 1 ? make_float2(cdp[0][o - 1], cdp[CH - 1][o - 1]) : make_float2(vx, vy);
       }
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        float a = 0.f;
+        float2 a2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int o = 0; o < K; ++o) a = fmaf(wk[K - 1 - o], dp[i + o], a);
-        dxv[i] = a;
+        for (int o = 0; o < K; ++o) a2 = ffma2(w2[K - 1 - o], dp2[i + o], a2);
+        dxv[0][i] = a2.x;
+        dxv[CH - 1][i] = a2.y;
+      }
+#pragma unroll
+      for (int k = 0; k < 8 + H; ++k) {
+        dp[0][k] = dp2[k].x;
+        dp[CH - 1][k] = dp2[k].y;
+      }
+      acc_b[0] = ab2.x;
+      acc_b[CH - 1] = ab2.y;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        acc_w[0][j] = aw2[j].x;
+        acc_w[CH - 1][j] = aw2[j].y;
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int t = t0 + i;
-        const int ci = min(p[i], t);  // tap o is kept iff o <= pos[t] and t - o >= 0
-        float pre = b;
+      for (int c = 0; c < CH; ++c) {
+        if (wheads) {
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-          if (K - 1 - j <= ci) pre = fmaf(wk[j], X[i + j], pre);
-        const float dpv = (t < te) ? gv[i] * (kSilu ? silu_grad_io<T>(pre) : 1.f) : 0.f;
-        dp[i] = dpv;
-        acc_b += dpv;
+          for (int i = 0; i < 8; ++i) {
+            const float pre = fmaf(wk[c][K - 1], xv[c][i], b[c]);
+            const float dpv = gv[c][i] * (kSilu ? silu_grad_io<T>(pre) : 1.f);
+            dp[c][i] = dpv;
+            acc_b[c] += dpv;
+            acc_w[c][K - 1] = fmaf(dpv, xv[c][i], acc_w[c][K - 1]);
+            dxv[c][i] = wk[c][K - 1] * dpv;
+          }
+        } else if (wfull) {
 #pragma unroll
-        for (int j = 0; j < K; ++j)
-          if (K - 1 - j <= ci) acc_w[j] = fmaf(dpv, X[i + j], acc_w[j]);
-      }
+          for (int i = 0; i < 8; ++i) {
+            float pre = b[c];
 #pragma unroll
-      for (int o = 1; o < K; ++o) {
-        const float vd = __shfl_down_sync(0xffffffffu, dp[o - 1], 1, G);
-        dp[8 + o - 1] = g == G - 1 ? cdp[o - 1] : vd;
-      }
+            for (int j = 0; j < K; ++j) pre = fmaf(wk[c][j], X[c][i + j], pre);
+            const float dpv = gv[c][i] * (kSilu ? silu_grad_io<T>(pre) : 1.f);
+            dp[c][i] = dpv;
+            acc_b[c] += dpv;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        float a = 0.f;
+            for (int j = 0; j < K; ++j) acc_w[c][j] = fmaf(dpv, X[c][i + j], acc_w[c][j]);
+          }
 #pragma unroll
-        for (int o = 0; o < K; ++o) {
-          // dp is 0 at and beyond L (own block: t >= te; carry: 0 past L)
-          const int pt = (i + o < 8) ? p[i + o] : ph[i + o - 8];
-          if (o <= pt) a = fmaf(wk[K - 1 - o], dp[i + o], a);
+          for (int o = 1; o < K; ++o) {
+            const float vd = __shfl_down_sync(0xffffffffu, dp[c][o - 1], 1, G);
+            dp[c][8 + o - 1] = g == G - 1 ? cdp[c][o - 1] : vd;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float a = 0.f;
+#pragma unroll
+            for (int o = 0; o < K; ++o) a = fmaf(wk[c][K - 1 - o], dp[c][i + o], a);
+            dxv[c][i] = a;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int t = t0 + i;
+            const int ci = min(p[i], t);  // tap o is kept iff o <= pos[t] and t - o >= 0
+            float pre = b[c];
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+              if (K - 1 - j <= ci) pre = fmaf(wk[c][j], X[c][i + j], pre);
+            const float dpv = (t < te) ? gv[c][i] * (kSilu ? silu_grad_io<T>(pre) : 1.f) : 0.f;
+            dp[c][i] = dpv;
+            acc_b[c] += dpv;
+#pragma unroll
+            for (int j = 0; j < K; ++j)
+              if (K - 1 - j <= ci) acc_w[c][j] = fmaf(dpv, X[c][i + j], acc_w[c][j]);
+          }
+#pragma unroll
+          for (int o = 1; o < K; ++o) {
+            const float vd = __shfl_down_sync(0xffffffffu, dp[c][o - 1], 1, G);
+            dp[c][8 + o - 1] = g == G - 1 ? cdp[c][o - 1] : vd;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float a = 0.f;
+#pragma unroll
+            for (int o = 0; o < K; ++o) {
+              // dp is 0 at and beyond L (own block: t >= te; carry: 0 past L)
+              const int pt = (i + o < 8) ? p[i + o] : ph[i + o - 8];
+              if (o <= pt) a = fmaf(wk[c][K - 1 - o], dp[c][i + o], a);
+            }
+            dxv[c][i] = a;
+          }
         }
-        dxv[i] = a;
       }
     }
     // next (earlier) iteration's carry = this block's first K-1 steps (lane g = 0)
 #pragma unroll
     for (int o = 1; o < K; ++o) {
-      cdp[o - 1] = __shfl_sync(0xffffffffu, dp[o - 1], 0, G);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) cdp[c][o - 1] = __shfl_sync(0xffffffffu, dp[c][o - 1], 0, G);
       cp[o - 1] = __shfl_sync(0xffffffffu, p[o - 1], 0, G);
     }
-    if (own) store8<T, kVec>(dxr, t0, tb, te, dxv);
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+      if (own[c]) store8<T, kVec>(dxr[c], t0, tb, te, dxv[c]);
   }
-  // one group reduction of (dw, db) for this (row, time range, channel)
+  // one warp reduction of (dw, db) per channel for this (row, time range)
 #pragma unroll
-  for (int j = 0; j <= K; ++j) {
-    float v = j < K ? acc_w[j] : acc_b;
+  for (int c = 0; c < CH; ++c) {
 #pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
-    if (g == 0 && own) ws[(((int64_t)r * ntc + tc) * Dn + d) * (K + 1) + j] = v;
+    for (int j = 0; j <= K; ++j) {
+      float v = j < K ? acc_w[c][j] : acc_b[c];
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+      if (g == 0 && own[c]) ws[(((int64_t)r * ntc + tc) * Dn + dd[c]) * (K + 1) + j] = v;
+    }
   }
 }
 
@@ -491,7 +636,7 @@ int conv_tspan(int64_t R, int64_t Dn, int64_t L, int chans, int span) {
 }
 int conv_ntc(int64_t L, int tspan) { return (int)((L + tspan - 1) / tspan); }
 int bwd_tspan(int64_t R, int64_t Dn, int64_t L) {
-  return conv_tspan(R, Dn, L, kConvBwdWarps, kSpan);
+  return conv_tspan(R, Dn, L, kConvBwdWarps * kConvBwdCh, kSpan);
 }
 
 bool a16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -531,7 +676,7 @@ pm_status bwd_launch(const void* x, const float* w, const float* b, const int32_
                      const void* dout, void* dx, float* dw, float* db, float* ws, int64_t R,
                      int64_t Dn, int64_t L, int silu, cudaStream_t s) {
   const int tspan = bwd_tspan(R, Dn, L), ntc = conv_ntc(L, tspan);
-  const int64_t per_cta = kConvBwdWarps;
+  const int64_t per_cta = (int64_t)kConvBwdWarps * kConvBwdCh;
   dim3 grid((unsigned)((Dn + per_cta - 1) / per_cta), (unsigned)R, (unsigned)ntc);
   if (silu)
     conv_bwd_kernel<T, K, V, true><<<grid, kConvBwdThreads, 0, s>>>(

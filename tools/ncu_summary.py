@@ -34,10 +34,10 @@ KEYS = {
 
 
 def kind(name):
-    for k in ("scan_bwd_finalize_bc", "scan_bwd_finalize_param", "scan_bwd_kernel", "scan_fwd",
+    for k in ("scan_bwd_finalize_bc", "scan_bwd_finalize_param", "scan_bwd_wide_kernel", "scan_bwd_kernel", "scan_fwd",
               "conv_bwd_finalize", "conv_bwd", "conv_fwd", "pack"):
         if k in name:
-            return {"scan_bwd_kernel": "scan_bwd", "scan_fwd": "scan_fwd", "conv_bwd": "conv_bwd",
+            return {"scan_bwd_kernel": "scan_bwd", "scan_bwd_wide_kernel": "scan_bwd", "scan_fwd": "scan_fwd", "conv_bwd": "conv_bwd",
                     "conv_fwd": "conv_fwd"}.get(k, k)
     return name
 
