@@ -301,11 +301,15 @@ PM_DEV float2 silu_grad2_io(float2 pre) {
   }
 }
 
-#ifndef PM_CONV_BWD_MINB  // resident conv bwd CTAs (warps) per SM the register allocation targets
-#define PM_CONV_BWD_MINB 1
+// (an explicit register target, PM_CONV_BWD_MINB=n: 20/24 warps per SM spill
+// and measured slower; n = 1 lets the allocator take 168 registers)
+#ifdef PM_CONV_BWD_MINB
+#define PM_CONV_BWD_BOUNDS __launch_bounds__(kConvBwdThreads, PM_CONV_BWD_MINB)
+#else
+#define PM_CONV_BWD_BOUNDS __launch_bounds__(kConvBwdThreads)
 #endif
 template <typename T, int K, bool kVec, bool kSilu>
-__global__ void __launch_bounds__(kConvBwdThreads, PM_CONV_BWD_MINB)
+__global__ void PM_CONV_BWD_BOUNDS
 conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                 const int32_t* __restrict__ pos, const T* __restrict__ dout, T* __restrict__ dx,
                 float* __restrict__ ws, int Dn, int L, int tspan, int ntc) {
