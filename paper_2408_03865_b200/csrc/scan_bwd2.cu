@@ -34,10 +34,6 @@ constexpr int kW2MinB = 2;                 // resident CTAs per SM (TMEM: 2 x 25
 #define PM_W2_UNROLL 2
 #endif
 constexpr int kW2AUnroll = PM_W2_AUNROLL;
-#ifndef PM_W2_ABPARK  // hot path parks {S_k, abar_k} of even steps instead of every state
-#define PM_W2_ABPARK 0
-#endif
-constexpr bool kAbPark = PM_W2_ABPARK;
 constexpr int kW2Unroll = PM_W2_UNROLL;
 
 template <typename T, int N>
@@ -114,15 +110,6 @@ PM_DEV void tmem_ld16_wait(uint32_t (&r)[16]) {
 // 16-byte store and copy the pairs into a register quad first)
 PM_DEV void sts64(uint32_t addr, float2 v) {
   asm volatile("st.shared.v2.f32 [%0], {%1, %2};\n" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
-}
-PM_DEV void tmem_ld32_wait(uint32_t (&r)[32]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
-                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]),
-                 "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]),
-                 "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]),
-                 "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]),
-                 "+r"(r[31]));
 }
 
 template <typename T, int N>
@@ -420,7 +407,7 @@ scan_bwd_wide_kernel(const __grid_constant__ ScanBwdArgs a) {
         }
       };
 
-      if (c0 == cb && c1 == cb + kChunk && hmask == 0u && !kAbPark) {
+      if (c0 == cb && c1 == cb + kChunk && hmask == 0u) {
         // ---- hot path: a full chunk without sequence heads: no per-step
         // head branch, so the scheduler interleaves the MUFU exponentials
         // with the FMA work around them.  Pass A parks the state entering
@@ -470,77 +457,6 @@ scan_bwd_wide_kernel(const __grid_constant__ ScanBwdArgs a) {
 #pragma unroll
             for (int p = 0; p < NP; ++p) h[c][p] = hp0[c][p];
           if (rs > 0) tmem_ld16_issue(tbase + (uint32_t)((k0 - 1) * 2 * NH), pre1);
-          reduce_round(rs, fdu, fddt);
-        }
-      } else if (c0 == cb && c1 == cb + kChunk && hmask == 0u) {
-        // ---- hot path: a full chunk without sequence heads.  Pass A parks,
-        // for every EVEN step k, the state entering it (S_k) and its abar_k
-        // in TMEM columns [16k, 16k+16) and [16k+16, 16k+32) -- the same 16
-        // columns per step as parking every state.  Pass B rebuilds the
-        // state entering the odd step k+1 as abar_k S_k + delta u B_k (the
-        // forward's own arithmetic: bit-identical) and takes abar_k from
-        // TMEM, so only odd steps evaluate an exponential: 1.5 instead of 2
-        // MUFU ex2 per element.  No per-step head branch, so the scheduler
-        // interleaves the exponentials with the FMA work around them.
-#pragma unroll kW2AUnroll
-        for (int ii = 0; ii < kChunk; ++ii) {
-          const float4 sv0 = P0[ii][jc0], sv1 = P1[ii][jc1];
-          const float2 dl2[2] = {f2(sv0.x), f2(sv1.x)};
-          const float2 dux2[2] = {f2(sv0.x * sv0.y), f2(sv1.x * sv1.y)};
-          const float2* Bt = reinterpret_cast<const float2*>(&sm.B[ii][n0]);
-          float2 ab[2][NP];
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int p = 0; p < NP; ++p) ab[c][p] = ex2x2(fmul2(dl2[c], A2[c][p]));
-          if ((ii & 1) == 0) {
-            tmem_st<2 * NH>(tbase + (uint32_t)(ii * 2 * NH), reinterpret_cast<const float*>(h));
-            tmem_st<2 * NH>(tbase + (uint32_t)((ii + 1) * 2 * NH), reinterpret_cast<const float*>(ab));
-          }
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int p = 0; p < NP; ++p) h[c][p] = ffma2(ab[c][p], h[c][p], fmul2(dux2[c], Bt[p]));
-        }
-        tmem_wait_st();
-        uint32_t pre[32];  // {S_k, abar_k} of the next round, loaded during the transposes
-        tmem_ld16_issue(tbase + (uint32_t)((kChunk - 2) * 2 * NH), *reinterpret_cast<uint32_t(*)[16]>(&pre[0]));
-        tmem_ld16_issue(tbase + (uint32_t)((kChunk - 1) * 2 * NH), *reinterpret_cast<uint32_t(*)[16]>(&pre[16]));
-        auto unpack = [&](const uint32_t* r, float2 (&v)[2][NP]) {
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int p = 0; p < NP; ++p)
-              v[c][p] = make_float2(__uint_as_float(r[c * NH + 2 * p]), __uint_as_float(r[c * NH + 2 * p + 1]));
-        };
-#pragma unroll kW2Unroll
-        for (int rs = kChunk / 2 - 1; rs >= 0; --rs) {
-          const int k0 = 2 * rs;  // the round's even step
-          tmem_ld32_wait(pre);
-          float2 S0[2][NP], ab0[2][NP], h1[2][NP], ab1[2][NP];
-          unpack(&pre[0], S0);
-          unpack(&pre[16], ab0);
-          {  // state entering the odd step: the forward's update of S0
-            const float4 sv0 = P0[k0][jc0], sv1 = P1[k0][jc1];
-            const float2 dux2[2] = {f2(sv0.x * sv0.y), f2(sv1.x * sv1.y)};
-            const float2* Bt = reinterpret_cast<const float2*>(&sm.B[k0][n0]);
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-              for (int p = 0; p < NP; ++p) h1[c][p] = ffma2(ab0[c][p], S0[c][p], fmul2(dux2[c], Bt[p]));
-          }
-          abar(k0 + 1, ab1);
-          float fdu[2], fddt[2];
-          bstep(k0 + 1, 1, false, h, h1, ab1, fdu[1], fddt[1]);
-          bstep(k0, 0, false, h1, S0, ab0, fdu[0], fddt[0]);
-#pragma unroll
-          for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int p = 0; p < NP; ++p) h[c][p] = S0[c][p];
-          if (rs > 0) {
-            tmem_ld16_issue(tbase + (uint32_t)((k0 - 2) * 2 * NH), *reinterpret_cast<uint32_t(*)[16]>(&pre[0]));
-            tmem_ld16_issue(tbase + (uint32_t)((k0 - 1) * 2 * NH), *reinterpret_cast<uint32_t(*)[16]>(&pre[16]));
-          }
           reduce_round(rs, fdu, fddt);
         }
       } else {
