@@ -150,6 +150,24 @@ def test_determinism():
         assert torch.equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("io", ["f32", "bf16"])
+def test_wide_backward_repeat_bit_identical(io):
+    """Race probe for the wide backward (compute-sanitizer is not available
+    on the GPU pool): its per-round warp transpose, the parked (du, ddt)
+    slots a lane pair shares, the TMA-staged raw buffer and the cross-warp
+    dB/dC sum are ordered only by warp / CTA barriers and the mbarrier; five
+    back-to-back runs over 4 rows x 2048 with every CTA slot busy must agree
+    bit for bit (a missing barrier shows up as run-to-run differences), and
+    the first run must match the oracle."""
+    rows, pos, valid, T, P = problem(4, 512, 2048, 16, 4, "random", io, seed=61)
+    ref = run_chain(pos, T, P)
+    check_chain(pos, T, P, ref, io)
+    for _ in range(4):
+        got = run_chain(pos, T, P)
+        for k in ("du", "ddt", "dA", "dB", "dC", "dD", "ddt_bias"):
+            assert torch.equal(got[k], ref[k]), k
+
+
 # --------------------------------------------------------------------------
 # P6: integer-exact regime -> bit-exact (A = 0, delta = 1, small integers)
 # --------------------------------------------------------------------------
