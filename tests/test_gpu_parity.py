@@ -168,6 +168,17 @@ def test_wide_backward_repeat_bit_identical(io):
             assert torch.equal(got[k], ref[k]), k
 
 
+@pytest.mark.parametrize("io,L", [("f32", 1020), ("f32", 772), ("bf16", 1000), ("bf16", 264)])
+def test_vector_path_ragged_range_end(io, L):
+    """Vector-path rows whose length is not a multiple of the 256-step conv
+    block (and, for fp32, ends mid 8-step vector: L % 8 == 4): the conv
+    backward's bulk-copied ring only holds the valid slots of the last block,
+    the rest must read as 0."""
+    rows, pos, valid, T, P = problem(2, 132, L, 16, 4, "edges", io, seed=71 + L)
+    out = run_chain(pos, T, P)
+    check_chain(pos, T, P, out, io)
+
+
 # --------------------------------------------------------------------------
 # P6: integer-exact regime -> bit-exact (A = 0, delta = 1, small integers)
 # --------------------------------------------------------------------------
