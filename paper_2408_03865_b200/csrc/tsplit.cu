@@ -21,7 +21,7 @@ namespace pm {
 namespace {
 
 constexpr int kTsThreads = 128;
-constexpr int kTsTile = 64;
+constexpr int kTsTile = 128;
 
 template <typename T, int N, bool kVec>
 PM_DEV void stage_c_tile(const T* __restrict__ C_r, int L, int j0, float (*sC)[N]) {
@@ -93,7 +93,15 @@ part_dh0(const int4* __restrict__ items, int P, const T* __restrict__ dt,
   const int64_t lane = ((int64_t)r * Dn + d) * L;
   const T* C_r = C + (int64_t)r * N * L;
   int j0 = -1;
-  for (int tb = s0 + ((fh - 1 - s0) & ~7); tb >= s0; tb -= 8) {
+  // dt / dout (/ z) of the next (earlier) 8 steps are in flight while these
+  // are computed (software pipeline: the walk is otherwise bound by one
+  // dependent global load per 8 steps)
+  const int tb_first = s0 + ((fh - 1 - s0) & ~7);
+  Raw8<T, kVec> pv, py, pz;
+  pv.load(dt + lane, tb_first, L);
+  py.load(dout + lane, tb_first, L);
+  if constexpr (kGate) pz.load(z + lane, tb_first, L);
+  for (int tb = tb_first; tb >= s0; tb -= 8) {
     if (j0 < 0 || tb < j0) {  // (CTA-uniform) the window holding tb
       j0 = tb & ~(kTsTile - 1);
       __syncthreads();
@@ -101,9 +109,14 @@ part_dh0(const int4* __restrict__ items, int P, const T* __restrict__ dt,
       __syncthreads();
     }
     float vv[8], yy[8], zz[8];
-    load8<T, kVec>(dt + lane, tb, L, vv);
-    load8<T, kVec>(dout + lane, tb, L, yy);
-    if constexpr (kGate) load8<T, kVec>(z + lane, tb, L, zz);
+    pv.unpack(vv);
+    py.unpack(yy);
+    if constexpr (kGate) pz.unpack(zz);
+    if (tb - 8 >= s0) {
+      pv.load(dt + lane, tb - 8, L);
+      py.load(dout + lane, tb - 8, L);
+      if constexpr (kGate) pz.load(z + lane, tb - 8, L);
+    }
 #pragma unroll
     for (int i = 7; i >= 0; --i) {
       const int t = tb + i;
