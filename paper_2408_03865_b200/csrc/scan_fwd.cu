@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(1024) seg_sort_kernel(const int4* __restrict__
 // S threads per channel (S = 1: all N states in one thread; S > 1, for
 // latency-bound launches: N/S states each, y summed over the S lanes by
 // shuffle -- a few long segments then run S times as many warps).
+#ifndef PM_FWD_TILE_PREFETCH
+#define PM_FWD_TILE_PREFETCH 1
+#endif
 template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh, int S = 1>
 __global__ void __launch_bounds__(kScanThreads, MinB)
 scan_fwd_kernel(const ScanFwdArgs a) {
@@ -243,12 +246,28 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   if (kGate) pz.load(z_row, tb, L);
   int j0 = -1;
   unsigned long long hmask = 0ull;
+  // Latency-bound launches (S > 1 lanes per channel): B/C/pos of the NEXT
+  // 64-step tile are loaded into registers a whole tile ahead, so the
+  // staging's global latency (ncu: ~14 % of the stall samples at the bf16
+  // conversions) overlaps the previous tile's steps -- 130m forward 0.443 ->
+  // 0.421 ms.  The one-lane-per-channel launch (1.4B) keeps the synchronous
+  // staging: at its 128-register cap the prefetch spills (0.808 -> 0.813 ms).
+  TileRegs<T, N, kTile, kVec> tr;
+  constexpr bool kTilePf = PM_FWD_TILE_PREFETCH != 0 && S > 1;
+  if constexpr (kTilePf) tr.fetch(B_r, C_r, pos_row, L, tb & ~(kTile - 1));
   for (; tb < s1; tb += 8) {
     if (j0 < 0 || (tb & (kTile - 1)) == 0) {  // CTA-uniform
       j0 = tb & ~(kTile - 1);
       __syncthreads();
-      stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask, a.h0 == nullptr);
+      if constexpr (kTilePf) {
+        tr.commit(L, j0, sB, sC, sMask, a.h0 == nullptr);
+      } else {
+        stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask, a.h0 == nullptr);
+      }
       __syncthreads();
+      if constexpr (kTilePf) {
+        if (j0 + kTile < s1) tr.fetch(B_r, C_r, pos_row, L, j0 + kTile);
+      }
       // head flags of the tile as a register bitmask (CTA-uniform): no
       // shared-memory load on the per-step critical path
       hmask = (unsigned long long)sMask[0] | ((unsigned long long)sMask[1] << 32);

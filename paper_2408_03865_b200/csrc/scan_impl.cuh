@@ -152,6 +152,66 @@ PM_DEV void stage_bc(const T* __restrict__ B_r, const T* __restrict__ C_r,
 }
 
 
+// The same staging split in two: tile_fetch() loads this thread's share of
+// the window [j0, j0 + W) into registers (issued a whole tile ahead, so the
+// global latency overlaps the previous tile's steps), tile_commit() converts
+// it into shared memory and builds the head mask (between the caller's two
+// barriers).  Shares: vector e = threadIdx.x (+ blockDim.x ...) of
+// N * W / 8 8-step vectors; warp 0 holds pos of W steps (W / 32 per lane).
+template <typename T, int N, int W, bool kVec>
+struct TileRegs {
+  static constexpr int kPer = (N * (W / 8) + 127) / 128;  // vectors per thread at 128 threads
+  Raw8<T, kVec> b[kPer], c[kPer];
+  int p[W / 32];
+  PM_DEV void fetch(const T* __restrict__ B_r, const T* __restrict__ C_r,
+                    const int32_t* __restrict__ pos_row, int L, int j0) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = threadIdx.x + k * blockDim.x;
+      if (e < N * (W / 8)) {
+        const int n = e % N, tb = (e / N) * 8;
+        b[k].load(B_r + (int64_t)n * L, j0 + tb, L);
+        c[k].load(C_r + (int64_t)n * L, j0 + tb, L);
+      }
+    }
+    if (threadIdx.x < 32) {
+#pragma unroll
+      for (int w = 0; w < W / 32; ++w) {
+        const int t = j0 + w * 32 + (int)threadIdx.x;
+        p[w] = t < L ? __ldg(pos_row + t) : 0;
+      }
+    }
+  }
+  template <int S>
+  PM_DEV void commit(int L, int j0, float (*sB)[S], float (*sC)[S], unsigned* sMask,
+                     bool t0_head) const {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int e = threadIdx.x + k * blockDim.x;
+      if (e < N * (W / 8)) {
+        const int n = e % N, tb = (e / N) * 8;
+        float vb[8], vc[8];
+        b[k].unpack(vb);
+        c[k].unpack(vc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          sB[tb + i][n] = vb[i];
+          sC[tb + i][n] = vc[i];
+        }
+      }
+    }
+    if (threadIdx.x < 32) {
+#pragma unroll
+      for (int w = 0; w < W / 32; ++w) {
+        const int t = j0 + w * 32 + (int)threadIdx.x;
+        const bool f = t >= L || (t == 0 && t0_head) || p[w] == 0;
+        const unsigned m = __ballot_sync(0xffffffffu, f);
+        if (threadIdx.x == 0) sMask[w] = m;
+      }
+    }
+  }
+};
+
 // ---------------------------------------------------------------------------
 // Raw inputs of one backward chunk of kBwdCh channels (shared by the backward kernel and its staging helper)
 template <typename T, int N, bool kGate>
