@@ -116,6 +116,9 @@ __global__ void __launch_bounds__(1024) seg_sort_kernel(const int4* __restrict__
 #ifndef PM_FWD_TILE_PREFETCH
 #define PM_FWD_TILE_PREFETCH 1
 #endif
+#ifndef PM_FWD_TILE_ASYNC
+#define PM_FWD_TILE_ASYNC 1
+#endif
 template <typename T, int N, bool kVec, int MinB, bool kGate, bool kZoh, int S = 1>
 __global__ void __launch_bounds__(kScanThreads, MinB)
 scan_fwd_kernel(const ScanFwdArgs a) {
@@ -132,6 +135,13 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   constexpr int kQv = (int)sizeof(T) / 2;  // 16-byte pieces per 8-element block
   static_assert((kRingDepth & (kRingDepth - 1)) == 0, "ring depth: power of 2");
   __shared__ __align__(16) uint4 ring[kRingDepth][2][kQv][kRing ? kScanThreads : 1];
+  // one-lane-per-channel vector path: the next tile's raw B/C/pos arrive by
+  // per-thread cp.async (issued right after a block's ring wait, so the next
+  // block's wait completes them), converted at the tile boundary
+  constexpr bool kTileAsync = kRing && S == 1 && PM_FWD_TILE_ASYNC != 0;
+  __shared__ __align__(16) T tB[kTileAsync ? N : 1][kTileAsync ? kTile : 8];
+  __shared__ __align__(16) T tC[kTileAsync ? N : 1][kTileAsync ? kTile : 8];
+  __shared__ __align__(16) int32_t tP[kTileAsync ? kTile : 4];
 
   const int L = a.L, Dn = a.Dn;
   const int ndblk = (Dn + kCh - 1) / kCh;
@@ -255,12 +265,60 @@ scan_fwd_kernel(const ScanFwdArgs a) {
   TileRegs<T, N, kTile, kVec> tr;
   constexpr bool kTilePf = PM_FWD_TILE_PREFETCH != 0 && S > 1;
   if constexpr (kTilePf) tr.fetch(B_r, C_r, pos_row, L, tb & ~(kTile - 1));
+  bool tile_pending = false;  // kTileAsync: the next tile's raw copies are to be issued
+  auto tile_issue = [&](int jn) {  // raw B/C/pos of the tile at jn (cp.async, own slots)
+    if constexpr (kTileAsync) {
+      constexpr int kE = 16 / (int)sizeof(T);  // elements per 16-byte piece
+      for (int e = threadIdx.x; e < 2 * N * (kTile / kE); e += blockDim.x) {
+        const int arr = e / (N * (kTile / kE)), rem = e % (N * (kTile / kE));
+        const int n = rem % N, q = rem / N;
+        const int t0 = jn + q * kE;
+        const int nb = t0 < L ? 16 : 0;  // (L % 4 == 0 on the vector path: whole pieces)
+        const T* src = (arr == 0 ? B_r : C_r) + (int64_t)n * L;
+        cp_async16(&(arr == 0 ? tB : tC)[n][q * kE], nb ? src + t0 : src, nb);
+      }
+      for (int e = threadIdx.x; e < kTile / 4; e += blockDim.x) {
+        const int t0 = jn + 4 * e;
+        const int nb = t0 < L ? 16 : 0;
+        cp_async16(&tP[4 * e], nb ? pos_row + t0 : pos_row, nb);
+      }
+      cp_async_commit();
+    }
+  };
   for (; tb < s1; tb += 8) {
     if (j0 < 0 || (tb & (kTile - 1)) == 0) {  // CTA-uniform
+      const bool first = j0 < 0;
       j0 = tb & ~(kTile - 1);
       __syncthreads();
       if constexpr (kTilePf) {
         tr.commit(L, j0, sB, sC, sMask, a.h0 == nullptr);
+      } else if constexpr (kTileAsync) {
+        if (first) {
+          stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask, a.h0 == nullptr);
+        } else {  // the raw tile was fetched during the previous tile
+          // (normally long complete; a segment that started late in the
+          // previous tile may have issued it one block ago -- the wait also
+          // covers this block's ring group, which the block needs anyway)
+          cp_async_wait<0>();
+          constexpr int kE = 16 / (int)sizeof(T);
+          for (int e = threadIdx.x; e < 2 * N * (kTile / kE); e += blockDim.x) {
+            const int arr = e / (N * (kTile / kE)), rem = e % (N * (kTile / kE));
+            const int n = rem % N, q = rem / N;
+#pragma unroll
+            for (int i = 0; i < kE; ++i)
+              (arr == 0 ? sB : sC)[q * kE + i][n] = IO<T>::cvt((arr == 0 ? tB : tC)[n][q * kE + i]);
+          }
+          __syncthreads();  // tP was written by other threads' copies (each waited on its own)
+          if (threadIdx.x < 32) {
+#pragma unroll
+            for (int w0 = 0; w0 < kTile; w0 += 32) {
+              const int t = j0 + w0 + (int)threadIdx.x;
+              const bool f = t >= L || (t == 0 && a.h0 == nullptr) || tP[w0 + threadIdx.x] == 0;
+              const unsigned m = __ballot_sync(0xffffffffu, f);
+              if (threadIdx.x == 0) sMask[w0 / 32] = m;
+            }
+          }
+        }
       } else {
         stage_bc<T, N, kTile, kVec>(B_r, C_r, pos_row, L, j0, sB, sC, sMask, a.h0 == nullptr);
       }
@@ -268,6 +326,7 @@ scan_fwd_kernel(const ScanFwdArgs a) {
       if constexpr (kTilePf) {
         if (j0 + kTile < s1) tr.fetch(B_r, C_r, pos_row, L, j0 + kTile);
       }
+      if constexpr (kTileAsync) tile_pending = j0 + kTile < s1;
       // head flags of the tile as a register bitmask (CTA-uniform): no
       // shared-memory load on the per-step critical path
       hmask = (unsigned long long)sMask[0] | ((unsigned long long)sMask[1] << 32);
@@ -276,6 +335,14 @@ scan_fwd_kernel(const ScanFwdArgs a) {
     if constexpr (kRing) {
       ring_issue(tb + 8 * (kRingDepth - 1));
       cp_async_wait<kRingDepth - 1>();  // this sub-block's group has landed
+      if constexpr (kTileAsync) {
+        // committed after this block's ring group: the next block's wait
+        // completes it (one 8-step block of latency cover, no stall here)
+        if (tile_pending) {
+          tile_issue(j0 + kTile);
+          tile_pending = false;
+        }
+      }
       const int sl = (tb >> 3) & (kRingDepth - 1);
       if constexpr (sizeof(T) == 2) {
         Raw8<T, kVec> ru, rt;
