@@ -112,6 +112,17 @@ part_dh0(const int4* __restrict__ items, int P, const T* __restrict__ dt,
     pv.unpack(vv);
     py.unpack(yy);
     if constexpr (kGate) pz.unpack(zz);
+    // delta of the 8 steps: the S lanes of a channel compute 8/S of them
+    // each and share them by shuffle (instead of all S lanes all 8)
+    float dls[8];
+    {
+      float mine[8 / S];
+#pragma unroll
+      for (int k = 0; k < 8 / S; ++k) mine[k] = delta_v(vv[part + S * k] + bias, softplus);
+      const int base = (int)(threadIdx.x & 31) & ~(S - 1);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) dls[i] = __shfl_sync(0xffffffffu, mine[i / S], base | (i % S));
+    }
     if (tb - 8 >= s0) {
       pv.load(dt + lane, tb - 8, L);
       py.load(dout + lane, tb - 8, L);
@@ -121,7 +132,7 @@ part_dh0(const int4* __restrict__ items, int P, const T* __restrict__ dt,
     for (int i = 7; i >= 0; --i) {
       const int t = tb + i;
       if (t >= fh) continue;  // CTA-uniform
-      const float delta = delta_v(vv[i] + bias, softplus);
+      const float delta = dls[i];
       float dyv = yy[i];
       if constexpr (kGate) dyv *= zz[i] * sigmoidf_fast(zz[i]);
       const float* Ct = sC[t - j0] + n0;
