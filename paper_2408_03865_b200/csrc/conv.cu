@@ -44,6 +44,14 @@ constexpr int kConvBwdWarps = PM_CONV_BWD_WARPS;
 #define PM_CONV_BWD_CH 2
 #endif
 constexpr int kConvBwdCh = PM_CONV_BWD_CH;
+// fp32 I/O keeps one channel per warp: its SiLU' is two MUFU ops per channel
+// anyway (no packed form), and one channel measured faster at the 130m shape
+// (0.065 vs 0.070 ms)
+#ifndef PM_CONV_BWD_CH_F32
+#define PM_CONV_BWD_CH_F32 1
+#endif
+template <typename T>
+constexpr int conv_bwd_ch() { return sizeof(T) == 2 ? kConvBwdCh : PM_CONV_BWD_CH_F32; }
 constexpr int kConvBwdThreads = 32 * kConvBwdWarps;
 constexpr int kCE = 8;                         // steps per lane per iteration
 constexpr int kSpan = 32 * kCE;                // steps per warp iteration
@@ -308,7 +316,7 @@ PM_DEV float2 silu_grad2_io(float2 pre) {
 #else
 #define PM_CONV_BWD_BOUNDS __launch_bounds__(kConvBwdThreads)
 #endif
-template <typename T, int K, bool kVec, bool kSilu>
+template <typename T, int K, bool kVec, bool kSilu, int CH>
 __global__ void PM_CONV_BWD_BOUNDS
 conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const float* __restrict__ bias,
                 const int32_t* __restrict__ pos, const T* __restrict__ dout, T* __restrict__ dx,
@@ -318,7 +326,7 @@ conv_bwd_kernel(const T* __restrict__ x, const float* __restrict__ w, const floa
   // indices, their halo and the tap decision, and the full-window path runs
   // the two channels as packed fp32x2 pairs (FFMA2: half the instructions,
   // no shifted operands to build)
-  constexpr int G = 32, CH = kConvBwdCh;
+  constexpr int G = 32;
   const int g = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int d0 = (blockIdx.x * kConvBwdWarps + wid) * CH;
   if (d0 >= Dn) return;  // warp-uniform
@@ -639,8 +647,8 @@ int conv_tspan(int64_t R, int64_t Dn, int64_t L, int chans, int span) {
   return (int)(blk_per * span);
 }
 int conv_ntc(int64_t L, int tspan) { return (int)((L + tspan - 1) / tspan); }
-int bwd_tspan(int64_t R, int64_t Dn, int64_t L) {
-  return conv_tspan(R, Dn, L, kConvBwdWarps * kConvBwdCh, kSpan);
+int bwd_tspan(int64_t R, int64_t Dn, int64_t L, int ch) {
+  return conv_tspan(R, Dn, L, kConvBwdWarps * ch, kSpan);
 }
 
 bool a16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -679,15 +687,16 @@ template <typename T, int K, bool V>
 pm_status bwd_launch(const void* x, const float* w, const float* b, const int32_t* pos,
                      const void* dout, void* dx, float* dw, float* db, float* ws, int64_t R,
                      int64_t Dn, int64_t L, int silu, cudaStream_t s) {
-  const int tspan = bwd_tspan(R, Dn, L), ntc = conv_ntc(L, tspan);
-  const int64_t per_cta = (int64_t)kConvBwdWarps * kConvBwdCh;
+  constexpr int CH = conv_bwd_ch<T>();
+  const int tspan = bwd_tspan(R, Dn, L, CH), ntc = conv_ntc(L, tspan);
+  const int64_t per_cta = (int64_t)kConvBwdWarps * CH;
   dim3 grid((unsigned)((Dn + per_cta - 1) / per_cta), (unsigned)R, (unsigned)ntc);
   if (silu)
-    conv_bwd_kernel<T, K, V, true><<<grid, kConvBwdThreads, 0, s>>>(
+    conv_bwd_kernel<T, K, V, true, CH><<<grid, kConvBwdThreads, 0, s>>>(
         static_cast<const T*>(x), w, b, pos, static_cast<const T*>(dout), static_cast<T*>(dx), ws,
         (int)Dn, (int)L, tspan, ntc);
   else
-    conv_bwd_kernel<T, K, V, false><<<grid, kConvBwdThreads, 0, s>>>(
+    conv_bwd_kernel<T, K, V, false, CH><<<grid, kConvBwdThreads, 0, s>>>(
         static_cast<const T*>(x), w, b, pos, static_cast<const T*>(dout), static_cast<T*>(dx), ws,
         (int)Dn, (int)L, tspan, ntc);
   PM_LAUNCH_CHECK();
@@ -746,7 +755,11 @@ pm_status pm_causal_conv1d_fwd(const void* x, const float* w, const float* bias,
 
 size_t pm_causal_conv1d_bwd_workspace(int64_t R, int64_t Dn, int64_t L, int32_t K) {
   if (R < 1 || Dn < 1 || L < 1 || K < 1 || K > 4) return 0;
-  return (size_t)R * conv_ntc(L, bwd_tspan(R, Dn, L)) * Dn * (K + 1) * sizeof(float);
+  // (the larger of the two launch shapes: fp32 and bf16 I/O may use
+  // different channels per warp, hence different time splits)
+  const int ntc = std::max(conv_ntc(L, bwd_tspan(R, Dn, L, conv_bwd_ch<float>())),
+                           conv_ntc(L, bwd_tspan(R, Dn, L, conv_bwd_ch<__nv_bfloat16>())));
+  return (size_t)R * ntc * Dn * (K + 1) * sizeof(float);
 }
 
 pm_status pm_causal_conv1d_bwd(const void* x, const float* w, const float* bias, const int32_t* pos,
